@@ -1,0 +1,526 @@
+"""CNT-GW outer solver on the GPU (reference ``solvers.py``).
+
+Public surface kept from the reference: ``EgwConfig`` / ``make_config``
+(solvers.py:44-110), ``SolveTrace`` (:113-151), ``EgwResult`` (:154-172),
+``SolverError`` (:40), ``random_gamma`` (:183), ``gamma_step`` (:190),
+``pi_step`` (:199), ``egw_objective`` (:259), ``solve_cnt_gw`` (:628) and
+``solve_adaptive`` (:652, feature-space solver only).
+
+One outer step (``_GwDevice.step``) is, entirely on the device:
+  K5  operator application  -> dot features for Gamma_t (E-side projection
+                               X_i.Gamma Y_j = (Gamma^T X_i).Y_j when D > E)
+  K1-K3 Sinkhorn loop at eps/8 with carried interaction potentials
+  K2  column tentative (only when the loop did not already produce it)
+  K4  fused plan pass: row masses, pi Y, pi s, argmax
+  K7  fp64 row/column reductions -> Gamma_{t+1}, KL terms, Err(pi)
+followed by one small device->host read of the reduced scalars (the stop rule
+and divergence guard of solvers.py:579-612 run on the host, as in the
+reference). The objective uses the potentials identity:
+  sum pi (f + g - C) = sum f~ r + sum g~ c + 2<Gamma_t, Gamma_{t+1}> - sum s^2 r
+                       - sum t^2 c + 2 sigma_ss
+with f~ = f - |X_i|^2 and g~ = g - |Gamma Y_j|^2 carried on device.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import divergence, engine
+from ._native import LIB, call
+from .measures import DenseCoupling, ImplicitCoupling
+from .sinkhorn import SinkhornConfig, SquaredEuclideanCost, sinkhorn
+
+MAX_DENSE_ENTRIES = 25_000_000
+ADAPTIVE_CAP = 2**14
+_DIVERGENCE_PATIENCE = 5
+INIT_KINDS = ("product", "random", "gamma", "coupling", "landmarks")
+
+
+class SolverError(RuntimeError):
+    """An outer solve failed (divergence, budget cap, degenerate state)."""
+
+
+@dataclass(frozen=True)
+class EgwConfig:
+    """Outer-loop configuration (reference solvers.py:44-94)."""
+
+    eps: float
+    inner: SinkhornConfig
+    max_outer: int = 200
+    delta_outer: float = 1e-5
+    init: str = "product"
+    init_gamma: np.ndarray | None = field(default=None, repr=False)
+    init_coupling: np.ndarray | None = field(default=None, repr=False)
+    init_pairs: np.ndarray | None = field(default=None, repr=False)
+    init_scale: float = 1.0
+    seed: int = 0
+    final_anneal: float | None = None
+    record_iterates: bool = False
+    max_dense_entries: int = MAX_DENSE_ENTRIES
+    feasibility_tol: float = 1e-4
+
+    def __post_init__(self):
+        checks = (
+            (self.eps > 0.0 and np.isfinite(self.eps), f"eps must be positive and finite, got {self.eps!r}"),
+            (self.max_outer >= 1, f"max_outer must be >= 1, got {self.max_outer!r}"),
+            (self.delta_outer > 0.0, f"delta_outer must be positive, got {self.delta_outer!r}"),
+            (self.init in INIT_KINDS, f"init must be one of {INIT_KINDS}, got {self.init!r}"),
+            (not (self.init == "gamma" and self.init_gamma is None), "init='gamma' needs init_gamma"),
+            (not (self.init == "coupling" and self.init_coupling is None),
+             "init='coupling' needs init_coupling"),
+            (not (self.init == "landmarks" and self.init_pairs is None),
+             "init='landmarks' needs init_pairs"),
+            (self.final_anneal is None or self.final_anneal > 0.0,
+             f"final_anneal must be positive, got {self.final_anneal!r}"),
+            (self.feasibility_tol > 0.0, f"feasibility_tol must be positive, got {self.feasibility_tol!r}"),
+        )
+        for ok, msg in checks:
+            if not ok:
+                raise ValueError(msg)
+
+
+def make_config(eps: float, *, mode: str = "symmetrized", n_inner: int | None = None,
+                threshold: float | None = None, max_inner: int = 10000, **kwargs) -> EgwConfig:
+    """Bundle the inner Sinkhorn configuration (reference solvers.py:97-110)."""
+    inner = SinkhornConfig(eps=eps, mode=mode, n_inner=n_inner, threshold=threshold,
+                           max_inner=max_inner)
+    return EgwConfig(eps=eps, inner=inner, **kwargs)
+
+
+_TRACE_COLS = ("steps", "objectives", "gamma_deltas", "marginal_errs", "inner_iters", "elapsed_s")
+
+
+@dataclass
+class SolveTrace:
+    """Per-outer-step log with the reference's CSV columns (solvers.py:113-151)."""
+
+    steps: list = field(default_factory=list)
+    objectives: list = field(default_factory=list)
+    gamma_deltas: list = field(default_factory=list)
+    marginal_errs: list = field(default_factory=list)
+    inner_iters: list = field(default_factory=list)
+    elapsed_s: list = field(default_factory=list)
+
+    def append(self, step, objective, gamma_delta, marginal_err, inner, elapsed):
+        vals = (int(step), float(objective), float(gamma_delta), float(marginal_err), int(inner),
+                float(elapsed))
+        for col, v in zip(_TRACE_COLS, vals):
+            getattr(self, col).append(v)
+
+    def __len__(self):
+        return len(self.steps)
+
+    def to_csv(self, path, header=None) -> None:
+        lines = [f"# {ln}" for ln in str(header).splitlines()] if header else []
+        lines.append("step,objective,gamma_delta,marginal_err,inner_iters,elapsed_s")
+        for s, o, d, e, k, t in zip(*(getattr(self, c) for c in _TRACE_COLS)):
+            lines.append(f"{s},{o:.17g},{d:.17g},{e:.17g},{k},{t:.6f}")
+        with open(path, "w", encoding="utf-8") as fh:
+            fh.write("\n".join(lines) + "\n")
+
+
+@dataclass
+class EgwResult:
+    """Outcome of an outer solve (solvers.py:154-172); ``argmax`` is the new
+    per-row argmax_j pi_ij of the returned coupling (lowest j on ties)."""
+
+    gamma: np.ndarray | None
+    coupling: object
+    trace: SolveTrace
+    value: float
+    converged: bool
+    iterates: list | None = None
+    schedule: list | None = None
+    coarse: "EgwResult | None" = None
+    argmax: np.ndarray | None = None
+
+
+@dataclass
+class _StepStats:
+    objective: float
+    gamma_delta: float
+    marginal_err: float
+    inner_iters: int
+
+
+def random_gamma(src, tgt, rng, scale: float = 1.0) -> np.ndarray:
+    """Gaussian operator at the canonical scale (solvers.py:183-187)."""
+    d, e = src.features.shape[1], tgt.features.shape[1]
+    tx = float(src.weights @ np.einsum("ij,ij->i", src.features, src.features))
+    ty = float(tgt.weights @ np.einsum("ij,ij->i", tgt.features, tgt.features))
+    return rng.standard_normal((d, e)) * (math.sqrt(tx * ty / (d * e)) * scale)
+
+
+def _half_sq(measure) -> np.ndarray:
+    h = getattr(measure, "half_sq_norms", None)
+    return 0.5 * np.einsum("ij,ij->i", measure.features, measure.features) if h is None else h
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+class _GwDevice:
+    """Device buffers and kernels of the feature-space CNT-GW step."""
+
+    def __init__(self, src, tgt, device):
+        self.device = device
+        x = np.asarray(src.features, dtype=np.float64)
+        y = np.asarray(tgt.features, dtype=np.float64)
+        self.n, self.d = x.shape
+        self.m, self.e = y.shape
+        self.x = engine.to_dev32(x, device)
+        self.y = engine.to_dev32(y, device)
+        self.x64 = engine.to_dev64(x, device)
+        self.y64 = engine.to_dev64(y, device)
+        self.sx = engine.to_dev32(_half_sq(src), device)
+        self.ty = engine.to_dev32(_half_sq(tgt), device)
+        self.sx64 = engine.to_dev64(_half_sq(src), device)
+        self.ty64 = engine.to_dev64(_half_sq(tgt), device)
+        self.a = engine.to_dev64(src.weights, device)
+        self.b = engine.to_dev64(tgt.weights, device)
+        self.proj_rows = self.d > self.e  # E-side projection
+        self.k = min(self.d, self.e)
+        self.kd = engine.padded_kd(self.k)
+        if self.proj_rows:
+            rows_feat = torch.zeros(self.n, self.kd, dtype=torch.float32, device=device)
+            cols_feat = engine.to_dev32(y, device, self.kd)
+        else:
+            rows_feat = engine.to_dev32(x, device, self.kd)
+            cols_feat = torch.zeros(self.m, self.kd, dtype=torch.float32, device=device)
+        log2a = torch.log2(self.a).float()
+        log2b = torch.log2(self.b).float()
+        self.src = engine.Side(rows_feat, self.sx, self.a, log2a)
+        self.tgt = engine.Side(cols_feat, self.ty, self.b, log2b)
+        self.fwd = engine.HalfUpdate(self.src, self.tgt, True)
+        self.bwd = engine.HalfUpdate(self.tgt, self.src, True)
+        self.loop = engine.SinkhornLoop(self.fwd, self.bwd, self.a, self.b, device)
+        self.proj_tmp = torch.empty(max(self.n, self.m) * self.k, dtype=torch.float32, device=device)
+        # K4 / K7 buffers
+        self.r = torch.empty(self.n, dtype=torch.float32, device=device)
+        self.pi_y = torch.empty(self.n * self.e, dtype=torch.float32, device=device)
+        self.pi_s = torch.empty(self.n, dtype=torch.float32, device=device)
+        self.argmax = torch.empty(self.n, dtype=torch.int64, device=device)
+        self.ws_plan = torch.empty(int(LIB.cntgw_plan_reduce_workspace(self.n, self.m, self.kd, 1, self.e)),
+                                   dtype=torch.uint8, device=device)
+        self.acc = torch.zeros(16 + self.d * self.e + 8, dtype=torch.float64, device=device)
+        ows = max(int(LIB.cntgw_outer_reduce_workspace(self.n, self.d, self.e)),
+                  int(LIB.cntgw_outer_reduce_workspace(self.m, 1, 1)))
+        self.ws_outer = torch.empty(ows, dtype=torch.uint8, device=device)
+        self.gamma_dev = torch.zeros(self.d * self.e, dtype=torch.float64, device=device)
+
+    # -- K5 -----------------------------------------------------------------
+    def set_gamma(self, gamma: np.ndarray):
+        g = torch.as_tensor(np.ascontiguousarray(gamma, dtype=np.float64), device=self.device)
+        if self.proj_rows:  # rows: Gamma^T X_i  (op = Gamma^T, E x D)
+            op, side, feat, count, din, dout = g.t().contiguous(), self.src, self.x, self.n, self.d, self.e
+        else:  # cols: Gamma Y_j  (op = Gamma, D x E)
+            op, side, feat, count, din, dout = g.contiguous(), self.tgt, self.y, self.m, self.e, self.d
+        self._op = op  # keep alive until the launch completes
+        if dout == self.kd:
+            out = side.feat
+        else:
+            out = self.proj_tmp[: count * dout]
+        call("cntgw_apply_operator", op.data_ptr(), dout, din, feat.data_ptr(), din, count,
+             out.data_ptr(), _stream())
+        if dout != self.kd:
+            side.feat[:, :dout].copy_(out.view(count, dout))
+
+    def col_sep(self, gamma) -> torch.Tensor:
+        """|Gamma Y_j|^2 in fp64 (reference separable column part)."""
+        g = torch.as_tensor(np.ascontiguousarray(gamma, dtype=np.float64), device=self.device)
+        return ((self.y64 @ g.t()) ** 2).sum(1)
+
+    def row_sep(self) -> torch.Tensor:
+        return (self.x64 ** 2).sum(1)
+
+    # -- one outer step ------------------------------------------------------
+    def step(self, f, g, gamma: np.ndarray, loop_cfg: engine.LoopConfig, eps_outer: float,
+             const: float, use_graph: bool):
+        self.set_gamma(gamma)
+        stats = self.loop.run(f, g, loop_cfg, use_graph=use_graph)
+        sym_break = stats.broke and loop_cfg.mode == "symmetrized"
+        if not sym_break:
+            self.loop.tentatives(f, g, need_f=False, need_g=True)
+        st = self.loop.state
+        self.fwd.pack(st, g)  # target records at the final lambda for the plan pass
+        stream = _stream()
+        call("cntgw_plan_reduce", st.ptr, self.kd, 1, self.e, self.src.feat.data_ptr(), self.kd,
+             self.sx.data_ptr(), f.data_ptr(), self.src.log2w.data_ptr(), self.fwd.rec.data_ptr(),
+             self.y.data_ptr(), self.e, self.ty.data_ptr(), self.n, self.m, self.r.data_ptr(),
+             self.pi_y.data_ptr(), self.pi_s.data_ptr(), self.argmax.data_ptr(),
+             self.ws_plan.data_ptr(), self.ws_plan.numel(), stream)
+        nrow = 16 + self.d * self.e
+        call("cntgw_outer_reduce_rows", self.x.data_ptr(), self.d, self.d, self.pi_y.data_ptr(),
+             self.e, self.r.data_ptr(), self.pi_s.data_ptr(), f.data_ptr(), self.sx.data_ptr(),
+             self.a.data_ptr(), self.n, self.acc.data_ptr(), self.ws_outer.data_ptr(),
+             self.ws_outer.numel(), stream)
+        call("cntgw_outer_reduce_cols", st.ptr, g.data_ptr(), self.loop.gt.data_ptr(),
+             self.ty.data_ptr(), self.b.data_ptr(), self.m, self.acc[nrow:].data_ptr(),
+             self.ws_outer.data_ptr(), self.ws_outer.numel(), stream)
+        acc = self.acc.cpu().numpy()  # the one host read per outer step
+        rows, cols = acc[:16], acc[nrow:]
+        gamma_next = acc[16:nrow].reshape(self.d, self.e).copy()
+        sigma_ss = rows[3]
+        cross = float((gamma * gamma_next).sum())
+        plan_lin = rows[0] + cols[0] + 2.0 * cross - rows[1] - cols[1] + 2.0 * sigma_ss
+        kl = plan_lin / stats.eps_eff
+        objective = const + 8.0 * (-float((gamma_next**2).sum()) + (eps_outer / 8.0) * kl
+                                   - 2.0 * sigma_ss)
+        err = rows[2] + cols[2]
+        delta = float(np.linalg.norm(gamma_next - gamma))
+        return gamma_next, _StepStats(objective, delta, err, stats.iterations), stats
+
+
+def _initial_gamma(src, tgt, cfg: EgwConfig) -> np.ndarray:
+    """Gamma_0 for each init kind (reference solvers.py:353-381)."""
+    x, y = np.asarray(src.features), np.asarray(tgt.features)
+    d, e = x.shape[1], y.shape[1]
+    if cfg.init == "product":
+        return np.zeros((d, e))
+    if cfg.init == "random":
+        return random_gamma(src, tgt, np.random.default_rng(cfg.seed), cfg.init_scale)
+    if cfg.init == "gamma":
+        gamma = np.asarray(cfg.init_gamma, dtype=np.float64)
+        if gamma.shape != (d, e):
+            raise ValueError(f"init_gamma shape {gamma.shape} does not match ({d}, {e})")
+        return np.array(gamma)
+    if cfg.init == "coupling":
+        pi = np.asarray(getattr(cfg.init_coupling, "matrix", cfg.init_coupling), dtype=np.float64)
+        if pi.shape != (x.shape[0], y.shape[0]):
+            raise ValueError(f"init_coupling shape {pi.shape} does not match ({x.shape[0]}, {y.shape[0]})")
+        dev = engine.require_cuda()
+        xt = torch.as_tensor(x, device=dev)
+        out = xt.t() @ (torch.as_tensor(pi, device=dev) @ torch.as_tensor(y, device=dev))
+        return out.cpu().numpy()
+    pairs = np.asarray(cfg.init_pairs)
+    if pairs.ndim != 2 or pairs.shape[1] != 2:
+        raise ValueError("init_pairs must be an array of (source, target) index pairs")
+    gamma = np.zeros((d, e))
+    for i, j in pairs:
+        if not (0 <= i < x.shape[0] and 0 <= j < y.shape[0]):
+            raise ValueError(f"landmark pair ({i}, {j}) out of range")
+        gamma += np.outer(x[int(i)], y[int(j)])
+    return gamma
+
+
+class _CntGwState:
+    """Feature-space alternate minimisation with device-resident plans
+    (reference solvers.py:285-350)."""
+
+    def __init__(self, src, tgt, cfg: EgwConfig, warm_potentials=None):
+        self.src, self.tgt, self.cfg = src, tgt, cfg
+        n, m = src.features.shape[0], tgt.features.shape[0]
+        if cfg.record_iterates and n * m > cfg.max_dense_entries:
+            raise ValueError(
+                f"recording iterates would densify {n * m} entries per step, "
+                f"beyond the memory guard ({cfg.max_dense_entries})"
+            )
+        self.device = engine.require_cuda()
+        self.dev = _GwDevice(src, tgt, self.device)
+        self.gamma = _initial_gamma(src, tgt, cfg)
+        if warm_potentials is None:
+            # interaction potentials 0 (solvers.py:297-301): f~ = s^2, g~ = t^2
+            self.f = (self.dev.sx64 ** 2).float()
+            self.g = (self.dev.ty64 ** 2).float()
+        else:
+            f0 = engine.to_dev64(np.asarray(warm_potentials[0], dtype=np.float64), self.device)
+            g0 = engine.to_dev64(np.asarray(warm_potentials[1], dtype=np.float64), self.device)
+            self.f = (f0 - self.dev.row_sep()).float()
+            self.g = (g0 - self.dev.col_sep(self.gamma)).float()
+        mx = divergence.moments(self.dev.x64, self.dev.a, self.device).cpu().numpy()
+        my = divergence.moments(self.dev.y64, self.dev.b, self.device).cpu().numpy()
+        self.constant = divergence.constant_from_moments(mx, self.dev.d, my, self.dev.e)
+        self.coupling_gamma = None
+        self.eps_eff = None
+        self.record = []
+        self.use_graph = self.dev.n * self.dev.m <= (1 << 24)
+
+    def step(self, inner_budget=None, anneal_from=None) -> _StepStats:
+        inner = self.cfg.inner
+        if inner_budget is not None:
+            inner = replace(inner, n_inner=inner_budget, threshold=None)
+        if anneal_from is not None:
+            inner = replace(inner, anneal_from=anneal_from)
+        loop_cfg = inner.with_temperature(self.cfg.eps / 8.0).loop_config()
+        gamma_t = self.gamma
+        gamma_next, stats, lstats = self.dev.step(self.f, self.g, gamma_t, loop_cfg, self.cfg.eps,
+                                                   self.constant, self.use_graph)
+        self.coupling_gamma = gamma_t
+        self.eps_eff = lstats.eps_eff
+        self.gamma = gamma_next
+        if self.cfg.record_iterates:
+            self.record.append(self.coupling().densify().matrix)
+        return stats
+
+    def coupling(self) -> ImplicitCoupling:
+        """The last plan (built on Gamma_t, solvers.py:326-336) in reference form."""
+        dev = self.dev
+        gt = self.coupling_gamma
+        f = (self.f.double() + dev.row_sep()).cpu().numpy()
+        g = (self.g.double() + dev.col_sep(gt)).cpu().numpy()
+        src, tgt = self.src, self.tgt
+        xbar = np.column_stack([src.features, _half_sq(src)])
+        zbar = np.column_stack([np.asarray(tgt.features) @ gt.T, _half_sq(tgt)])
+        cp = ImplicitCoupling(f, g, SquaredEuclideanCost(xbar, zbar), src.weights, tgt.weights,
+                              self.eps_eff, device=(self.f, self.g, dev))
+        return cp
+
+    def result(self, trace, converged, schedule=None) -> EgwResult:
+        coupling = self.coupling() if self.coupling_gamma is not None else None
+        return EgwResult(
+            gamma=self.gamma, coupling=coupling, trace=trace,
+            value=trace.objectives[-1] if len(trace) else math.nan, converged=converged,
+            iterates=self.record if self.cfg.record_iterates else None, schedule=schedule,
+            argmax=self.dev.argmax.cpu().numpy() if coupling is not None else None,
+        )
+
+
+def _run_outer(state, cfg: EgwConfig, adaptive: bool = False) -> EgwResult:
+    """Outer control: trace, |dobj| stop, 5-increase guard, adaptive doubling,
+    optional final annealed step (reference solvers.py:556-625)."""
+    trace = SolveTrace()
+    start = time.perf_counter()
+    prev, schedule, budget = None, [], None
+    if adaptive:
+        if cfg.inner.n_inner is None:
+            raise ValueError("the adaptive wrapper needs a fixed-budget inner configuration")
+        budget = cfg.inner.n_inner
+    ups, converged = 0, False
+    for k in range(1, cfg.max_outer + 1):
+        stats = state.step(inner_budget=budget)
+        schedule.append(budget if adaptive else stats.inner_iters)
+        trace.append(k, stats.objective, stats.gamma_delta, stats.marginal_err, stats.inner_iters,
+                     time.perf_counter() - start)
+        if prev is not None:
+            change = prev - stats.objective
+            if abs(change) < cfg.delta_outer and not (adaptive and stats.marginal_err > cfg.feasibility_tol):
+                converged = True
+                prev = stats.objective
+                break
+            if change < 0.0:
+                if adaptive:
+                    budget *= 2
+                    if budget > ADAPTIVE_CAP:
+                        raise SolverError(
+                            f"adaptive inner budget exceeded the cap ({ADAPTIVE_CAP}); "
+                            "the objective keeps increasing, likely a non-CNT cost or "
+                            "a temperature too small for this instance"
+                        )
+                    prev = stats.objective
+                    continue
+                ups += 1
+                if ups >= _DIVERGENCE_PATIENCE:
+                    raise SolverError(
+                        f"objective increased {_DIVERGENCE_PATIENCE} outer steps in a "
+                        "row; raise n_inner or use the adaptive wrapper"
+                    )
+            else:
+                ups = 0
+        prev = stats.objective
+    if cfg.final_anneal is not None:
+        stats = state.step(inner_budget=budget, anneal_from=cfg.final_anneal)
+        trace.append(len(trace) + 1, stats.objective, stats.gamma_delta, stats.marginal_err,
+                     stats.inner_iters, time.perf_counter() - start)
+        if adaptive:
+            schedule.append(budget)
+    return state.result(trace, converged, schedule=schedule if adaptive else None)
+
+
+def solve_cnt_gw(src, tgt, cfg: EgwConfig, _warm_potentials=None) -> EgwResult:
+    """Feature-space EGW solve (reference solvers.py:628-632)."""
+    return _run_outer(_CntGwState(src, tgt, cfg, warm_potentials=_warm_potentials), cfg)
+
+
+def solve_adaptive(solver, *args, cfg: EgwConfig) -> EgwResult:
+    """Inner-budget doubling wrapper (reference solvers.py:652-665); the GPU
+    build serves the feature-space solver only."""
+    if solver is not solve_cnt_gw:
+        raise ValueError("solver must be solve_cnt_gw (dense solver families are out of scope)")
+    return _run_outer(_CntGwState(*args, cfg), cfg, adaptive=True)
+
+
+# ---------------------------------------------------------------------------
+# building blocks exposed by the reference API
+# ---------------------------------------------------------------------------
+def pi_step(gamma, src, tgt, eps: float, inner: SinkhornConfig):
+    """Plan update: EOT between augmented features at eps/8 (solvers.py:199-224)."""
+    zbar = np.column_stack([np.asarray(tgt.features) @ np.asarray(gamma).T, _half_sq(tgt)])
+    xbar = np.column_stack([src.features, _half_sq(src)])
+    cost = SquaredEuclideanCost(xbar, zbar)
+    if inner.warm_start is None:
+        inner = inner.with_warm_start((xbar**2).sum(axis=1), (zbar**2).sum(axis=1))
+    return sinkhorn(src.weights, tgt.weights, cost, inner.with_temperature(eps / 8.0))
+
+
+def _plan_pass(coupling, src, tgt):
+    """Fused K4 pass over an ImplicitCoupling on a SquaredEuclideanCost
+    (augmented features): returns device (r, pi Y, pi s, argmax)."""
+    cost = coupling.cost
+    if not isinstance(cost, SquaredEuclideanCost):
+        raise TypeError("fused plan reductions need a SquaredEuclideanCost coupling")
+    dev = engine.require_cuda()
+    x, z = cost._x, cost._z
+    xf, zf = x[:, :-1], z[:, :-1]
+    kd = engine.padded_kd(max(1, xf.shape[1]))
+    e = np.asarray(tgt.features).shape[1]
+    from .sinkhorn import feature_problem
+
+    srcs, tgts, fwd, _ = feature_problem(xf, x[:, -1], zf, z[:, -1], coupling.source_weights,
+                                         coupling.target_weights, dev)
+    f = engine.to_dev32(coupling.f - (xf * xf).sum(1), dev)
+    g = engine.to_dev32(coupling.g - (zf * zf).sum(1), dev)
+    st = engine.SweepState(dev)
+    st.init(coupling.eps_eff)
+    fwd.pack(st, g)
+    n, m = cost.shape
+    r = torch.empty(n, dtype=torch.float32, device=dev)
+    pi_y = torch.empty(n * e, dtype=torch.float32, device=dev)
+    pi_s = torch.empty(n, dtype=torch.float32, device=dev)
+    am = torch.empty(n, dtype=torch.int64, device=dev)
+    ws = torch.empty(int(LIB.cntgw_plan_reduce_workspace(n, m, kd, 1, e)), dtype=torch.uint8, device=dev)
+    y = engine.to_dev32(tgt.features, dev)
+    ty = engine.to_dev32(_half_sq(tgt), dev)
+    call("cntgw_plan_reduce", st.ptr, kd, 1, e, srcs.feat.data_ptr(), kd, srcs.sq.data_ptr(),
+         f.data_ptr(), srcs.log2w.data_ptr(), fwd.rec.data_ptr(), y.data_ptr(), e, ty.data_ptr(),
+         n, m, r.data_ptr(), pi_y.data_ptr(), pi_s.data_ptr(), am.data_ptr(), ws.data_ptr(),
+         ws.numel(), _stream())
+    return r, pi_y.view(n, e), pi_s, am
+
+
+def gamma_step(coupling, src, tgt) -> np.ndarray:
+    """Gamma = X^T pi Y with the plan kept implicit (solvers.py:190-196)."""
+    if isinstance(coupling, DenseCoupling):
+        dev = engine.require_cuda()
+        pi = torch.as_tensor(coupling.matrix, device=dev)
+        xt = torch.as_tensor(np.asarray(src.features), device=dev)
+        return (xt.t() @ (pi @ torch.as_tensor(np.asarray(tgt.features), device=dev))).cpu().numpy()
+    _, pi_y, _, _ = _plan_pass(coupling, src, tgt)
+    x = torch.as_tensor(np.asarray(src.features), device=pi_y.device)
+    return (x.t() @ pi_y.double()).cpu().numpy()
+
+
+def egw_objective(gamma, coupling, src, tgt, eps: float) -> float:
+    """C + 8 F(Gamma, pi) for any operator/plan pair (solvers.py:259-282)."""
+    from .measures import kl_divergence
+
+    gamma = np.asarray(gamma, dtype=np.float64)
+    if isinstance(coupling, ImplicitCoupling):
+        r, pi_y, pi_s, _ = _plan_pass(coupling, src, tgt)
+        x = torch.as_tensor(np.asarray(src.features), device=pi_y.device)
+        xt_pi_y = (x.t() @ pi_y.double()).cpu().numpy()
+        sigma_ss = float((torch.as_tensor(_half_sq(src), device=pi_y.device) * pi_s.double()).sum())
+        kl = kl_divergence(coupling)
+    else:
+        pi = coupling.matrix
+        xt_pi_y = np.asarray(src.features).T @ (pi @ np.asarray(tgt.features))
+        sigma_ss = float(_half_sq(src) @ pi @ _half_sq(tgt))
+        kl = kl_divergence(coupling)
+    cross = float((gamma * xt_pi_y).sum()) + sigma_ss
+    const = divergence.constant_value(src, tgt)
+    return const + 8.0 * (float((gamma**2).sum()) + (eps / 8.0) * kl - 2.0 * cross)
