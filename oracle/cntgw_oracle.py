@@ -84,18 +84,19 @@ class LowRank:
 # ----------------------------------------------------------------------------
 # half-update and gaps (sinkhorn.py:166-188)
 # ----------------------------------------------------------------------------
-def softmin(cost, log_w, pot, eps, row_idx=None, threads=1):
+def softmin(cost, log_w, pot, eps, row_idx=None, threads=1, block=BLOCK):
     """out_i = -eps * logsumexp_j(log_w_j + (pot_j - C_ij)/eps)  (sinkhorn.py:166-176).
 
     ``row_idx`` restricts the evaluation to a subset of rows (used for the
-    full-size subsample parity checks); ``threads`` splits the 1024-row blocks
-    over a thread pool (numpy/BLAS release the GIL), which is how the CPU
-    baseline uses the host's cores.
+    full-size subsample parity checks); ``threads`` splits the row blocks over
+    a thread pool (numpy/BLAS release the GIL), which is how the CPU baseline
+    uses the host's cores; ``block`` (default the reference's 1024 rows) bounds
+    the per-block memory (block x M doubles) when many threads run at once.
     """
     bias = np.asarray(log_w, dtype=np.float64) + np.asarray(pot, dtype=np.float64) / eps
     n = cost.shape[0]
     if row_idx is None:
-        spans = [(i0, min(i0 + BLOCK, n)) for i0 in range(0, n, BLOCK)]
+        spans = [(i0, min(i0 + block, n)) for i0 in range(0, n, block)]
         out = np.empty(n)
 
         def run(span):
@@ -104,7 +105,7 @@ def softmin(cost, log_w, pot, eps, row_idx=None, threads=1):
     else:
         row_idx = np.asarray(row_idx)
         out = np.empty(row_idx.size)
-        spans = [(k, min(k + BLOCK, row_idx.size)) for k in range(0, row_idx.size, BLOCK)]
+        spans = [(k, min(k + block, row_idx.size)) for k in range(0, row_idx.size, block)]
 
         def run(span):
             k0, k1 = span

@@ -24,39 +24,43 @@ class SweepStateStruct(ctypes.Structure):
     _fields_ = [
         ("eps", c_double), ("anneal_from", c_double), ("threshold", c_double),
         ("eps_n", c_double), ("gap_r", c_double), ("gap_c", c_double),
-        ("lam", c_float), ("inv_lam", c_float), ("sqrt_lam", c_float),
+        ("lam_d", c_double), ("sqrt_lam_d", c_double),
+        ("lam", c_float), ("sqrt_lam", c_float),
         ("max_sweeps", ctypes.c_int32), ("mode", ctypes.c_int32), ("sweep", ctypes.c_int32),
         ("applied", ctypes.c_int32), ("done", ctypes.c_int32), ("converged", ctypes.c_int32),
-        ("check", ctypes.c_int32), ("pad_", ctypes.c_int32 * 2),
+        ("check", ctypes.c_int32), ("pad_", ctypes.c_int32),
     ]
 
+
+F32, F64 = 0, 1  # cntgw_precision
 
 # name -> (restype, argtypes); every symbol include/cntgw_b200.h declares
 SIGNATURES = {
     "cntgw_abi_version": (c_int, []),
     "cntgw_last_error": (ctypes.c_char_p, []),
     "cntgw_sweep_state_size": (c_int, []),
-    "cntgw_col_stride": (c_int, [c_int, c_int]),
+    "cntgw_col_stride": (c_int, [c_int, c_int, c_int]),
     "cntgw_cols_padded": (c_i64, [c_i64]),
     "cntgw_sweep_init": (c_int, [c_vp, c_double, c_double, c_double, c_int, c_int, c_vp]),
     "cntgw_sweep_begin": (c_int, [c_vp, c_vp]),
     "cntgw_gap_blocks": (c_int, [c_i64]),
-    "cntgw_sweep_gap": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "cntgw_sweep_gap": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "cntgw_sweep_finish": (c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "cntgw_sweep_apply": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp]),
-    "cntgw_prep_cols": (c_int, [c_vp, c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp,
-                                c_vp]),
-    "cntgw_softmin_workspace": (c_size_t, [c_i64, c_i64, c_int, c_int]),
-    "cntgw_softmin": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64,
-                              c_i64, c_vp, c_vp, c_vp, c_vp, c_size_t, c_vp]),
-    "cntgw_lse_finalize": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "cntgw_prep_cols": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64,
+                                c_vp, c_vp]),
+    "cntgw_softmin_workspace": (c_size_t, [c_int, c_i64, c_i64, c_int, c_int]),
+    "cntgw_softmin": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_vp,
+                              c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_size_t, c_vp]),
+    "cntgw_lse_finalize": (c_int, [c_vp, c_int, c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "cntgw_softmin_dense": (c_int, [c_vp, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64,
                                     c_vp, c_vp]),
-    "cntgw_plan_reduce_workspace": (c_size_t, [c_i64, c_i64, c_int, c_int, c_int]),
-    "cntgw_plan_reduce": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp,
-                                  c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
+    "cntgw_plan_reduce_workspace": (c_size_t, [c_i64, c_i64, c_int, c_int]),
+    "cntgw_plan_reduce": (c_int, [c_vp, c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                  c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
                                   c_size_t, c_vp]),
-    "cntgw_apply_operator": (c_int, [c_vp, c_int, c_int, c_vp, c_i64, c_i64, c_vp, c_vp]),
+    "cntgw_apply_operator": (c_int, [c_vp, c_int, c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64,
+                                     c_vp]),
     "cntgw_outer_reduce_workspace": (c_size_t, [c_i64, c_int, c_int]),
     "cntgw_outer_reduce_rows": (c_int, [c_vp, c_i64, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp,
                                         c_vp, c_i64, c_vp, c_vp, c_size_t, c_vp]),
@@ -82,7 +86,7 @@ def _load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.cntgw_abi_version() != 1:
+    if lib.cntgw_abi_version() != 2:
         raise ImportError("libcntgw_b200.so ABI version mismatch; rebuild the extension")
     if lib.cntgw_sweep_state_size() != ctypes.sizeof(SweepStateStruct):
         raise ImportError("cntgw_sweep_state layout mismatch between header and host mirror")

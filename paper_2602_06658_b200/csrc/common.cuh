@@ -9,7 +9,6 @@
 
 namespace cntgw {
 
-constexpr float kLog2e = 1.4426950408889634f;
 constexpr double kLog2eD = 1.4426950408889634;
 constexpr double kLn2D = 0.6931471805599453;
 
@@ -17,16 +16,31 @@ constexpr double kLn2D = 0.6931471805599453;
 // are padded to a multiple of this so every tile is full.
 constexpr int kColTile = 256;
 
+// Finite sentinels of the fp64 path (the ALU double->float conversion below
+// is valid for |v| < 2^127): padding columns carry -beta = +kPadQ, and a
+// row's reference starts at kStartQ > kPadQ so the first group rebases.
+constexpr double kPadQ = 1.0e30;
+constexpr double kStartQ = 3.0e30;
+
+// Lazy-rebase trigger: a group of G terms summing above 2^16 (or inf/NaN).
+constexpr float kRebase = 65536.0f;
+
 // MUFU.EX2 without range fix-up (flush-to-zero); argument in log2 units.
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ float lg2(float x) {
-  float y;
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
+
+// double -> float on the integer ALU pipe (truncating the mantissa), so the
+// fp64 path does not spend a second XU-pipe op (F2F shares the pipe with
+// MUFU.EX2, measured 16/clk/SM). |v| is clamped below at 2^-126.
+__device__ __forceinline__ float f64_to_f32_alu(double v) {
+  const uint32_t lo = (uint32_t)__double2loint(v);
+  const uint32_t hi = (uint32_t)__double2hiint(v);
+  const uint32_t mag = max(hi & 0x7fffffffu, 0x38100000u);
+  const uint32_t f = __funnelshift_l(lo, mag - 0x38000000u, 3);
+  return __uint_as_float((f & 0x7fffffffu) | (hi & 0x80000000u));
 }
 
 // Packed fp32x2 arithmetic (sm_100a FFMA2/FADD2): two rows per instruction.
@@ -81,6 +95,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+
+// Double-buffered streaming of fixed-size column tiles through shared memory:
+// thread 0 issues the bulk copies, every thread waits on the stage barrier.
+struct TilePipe {
+  uint64_t* bars;
+  __device__ void init() {
+    if (threadIdx.x == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
+};
 
 __device__ __forceinline__ bool skip_now(const cntgw_sweep_state* st, int skip_if_done) {
   return skip_if_done && st != nullptr && st->done;

@@ -12,109 +12,104 @@
 #pragma once
 
 #include "common.cuh"
-#include "softmin_fma.cuh"
+#include "softmin.cuh"
 
 namespace cntgw {
 
 struct PlanReduceArgs {
   const cntgw_sweep_state* st;
-  const float* row_feat;
+  const double* row_feat;
   int64_t ld_row;
-  const float* row_sq;
-  const float* f_tilde;
-  const float* log2a;
-  const float* col_rec;  // packed q-records (cntgw_prep_cols)
-  const float* col_acc;  // packed [Y (E) | s | pad] records, stride EA
+  const double* row_sq;
+  const double* f_tilde;
+  const double* log2a;
+  const double* col_rec;  // packed fp64 q-records (cntgw_prep_cols, CNTGW_F64, sq=1)
+  const double* col_acc;  // packed [Y (E) | s | pad] fp64 records, stride AccLayout<E>
   int64_t n, m;
-  float* row_mass;
-  float* pi_y;  // n x e_real
+  double* row_mass;
+  double* pi_y;  // n x e_real
   int e_real;
-  float* pi_s;
+  double* pi_s;
   int64_t* argmax;
 };
 
 template <int E>
 struct AccLayout {
-  static constexpr int kStride = (E + 1 + 3) / 4 * 4;
+  static constexpr int kStride = (E + 1 + 1) / 2 * 2;  // doubles, 16-byte multiple
 };
 
-template <int KD, int SQ, int E, int G>
-static __global__ void __launch_bounds__(128) plan_reduce_kernel(const PlanReduceArgs a) {
-  using L = ColLayout<KD, SQ>;
+// One fp64 pass per row: mass, pi Y, pi s and argmax against a lazily
+// rebased reference (same scheme as the fp64 softmin).
+template <int KD, int E, int G, int TILE>
+__global__ void __launch_bounds__(128) plan_reduce_kernel(const PlanReduceArgs a) {
+  using L = ColLayout<double, KD, 1>;
   using A = AccLayout<E>;
-  constexpr int kRecF = kColTile * L::kStride;
-  constexpr int kAccF = kColTile * A::kStride;
-  extern __shared__ __align__(128) float smem[];
+  constexpr int kRecN = TILE * L::kStride;
+  constexpr int kAccN = TILE * A::kStride;
+  extern __shared__ __align__(128) double smem_r[];
   __shared__ uint64_t bars[2];
 
   const int64_t i = (int64_t)blockIdx.x * 128 + threadIdx.x;
   const bool live = i < a.n;
-  const float sl = a.st->sqrt_lam;
-  float x[KD];
+  double x[KD];
 #pragma unroll
-  for (int k = 0; k < KD; ++k) x[k] = live ? a.row_feat[i * a.ld_row + k] : 0.f;
-  const float s = (SQ && live) ? sl * a.row_sq[i] : 0.f;
+  for (int k = 0; k < KD; ++k) x[k] = live ? a.row_feat[i * a.ld_row + k] : 0.0;
+  const double s = live ? a.st->sqrt_lam_d * a.row_sq[i] : 0.0;
 
-  float mq = CUDART_INF_F, S = 0.f, acc_s = 0.f, qbest = CUDART_INF_F;
-  float acc_y[E];
+  double mq = kStartQ, S = 0.0, acc_s = 0.0, qbest = CUDART_INF;
+  double acc_y[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) acc_y[e] = 0.f;
+  for (int e = 0; e < E; ++e) acc_y[e] = 0.0;
   int64_t jbest = 0;
 
   const int64_t mpad = (a.m + kColTile - 1) / kColTile * kColTile;
-  const int ntiles = (int)(mpad / kColTile);
-  const uint32_t rec_bytes = kRecF * sizeof(float), acc_bytes = kAccF * sizeof(float);
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  auto issue = [&](int t, int s_) {
-    float* base = smem + s_ * (kRecF + kAccF);
-    mbar_expect_tx(&bars[s_], rec_bytes + acc_bytes);
-    bulk_g2s(base, a.col_rec + (int64_t)t * kRecF, rec_bytes, &bars[s_]);
-    bulk_g2s(base + kRecF, a.col_acc + (int64_t)t * kAccF, acc_bytes, &bars[s_]);
+  const int ntiles = (int)(mpad / TILE);
+  const uint32_t rec_bytes = kRecN * sizeof(double), acc_bytes = kAccN * sizeof(double);
+  TilePipe pipe{bars};
+  pipe.init();
+  auto issue = [&](int t, int sb) {
+    double* base = smem_r + sb * (kRecN + kAccN);
+    mbar_expect_tx(&bars[sb], rec_bytes + acc_bytes);
+    bulk_g2s(base, a.col_rec + (int64_t)t * kRecN, rec_bytes, &bars[sb]);
+    bulk_g2s(base + kRecN, a.col_acc + (int64_t)t * kAccN, acc_bytes, &bars[sb]);
   };
   if (threadIdx.x == 0)
-    for (int s_ = 0; s_ < 2 && s_ < ntiles; ++s_) issue(s_, s_);
+    for (int sb = 0; sb < 2 && sb < ntiles; ++sb) issue(sb, sb);
 
   for (int t = 0; t < ntiles; ++t) {
     const int sb = t & 1;
     mbar_wait(&bars[sb], (t >> 1) & 1);
-    const float* rec = smem + sb * (kRecF + kAccF);
-    const float* acr = rec + kRecF;
+    const double* rec = smem_r + sb * (kRecN + kAccN);
+    const double* acr = rec + kRecN;
 #pragma unroll 1
-    for (int j = 0; j < kColTile; j += G) {
-      float q[G];
+    for (int j = 0; j < TILE; j += G) {
+      double q[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        const float* c = rec + (j + g) * L::kStride;
-        float acc = c[L::kBeta];
+        const double* c = rec + (j + g) * L::kStride;
+        double acc = c[L::kBeta];
 #pragma unroll
-        for (int k = 0; k < KD; ++k) acc = fmaf(x[k], c[k], acc);
-        if (SQ) {
-          const float u = s + c[KD];
-          acc = fmaf(u, u, acc);
-        }
+        for (int k = 0; k < KD; ++k) acc = fma(x[k], c[k], acc);
+        const double u = s + c[KD];
+        acc = fma(u, u, acc);
         q[g] = acc;
-        if (acc < qbest) {  // strict: first (lowest) j wins ties, numpy.argmax convention
+        if (acc < qbest) {  // strict: the first (lowest) j wins ties, numpy.argmax rule
           qbest = acc;
-          jbest = (int64_t)t * kColTile + j + g;
+          jbest = (int64_t)t * TILE + j + g;
         }
       }
       float ev[G], gs = 0.f;
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        ev[g] = ex2(mq - q[g]);
+        ev[g] = ex2(f64_to_f32_alu(mq - q[g]));
         gs += ev[g];
       }
       if (!(gs <= kRebase)) {
-        float qmin = q[0];
+        double qmin = q[0];
 #pragma unroll
-        for (int g = 1; g < G; ++g) qmin = fminf(qmin, q[g]);
+        for (int g = 1; g < G; ++g) qmin = fmin(qmin, q[g]);
         if (qmin < mq) {
-          const float sc = ex2(qmin - mq);
+          const double sc = exp2(qmin - mq);
           S *= sc;
           acc_s *= sc;
 #pragma unroll
@@ -122,23 +117,24 @@ static __global__ void __launch_bounds__(128) plan_reduce_kernel(const PlanReduc
           mq = qmin;
         }
 #pragma unroll
-        for (int g = 0; g < G; ++g) ev[g] = ex2(mq - q[g]);
+        for (int g = 0; g < G; ++g) ev[g] = ex2(f64_to_f32_alu(mq - q[g]));
       }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        const float* y = acr + (j + g) * A::kStride;
-        S += ev[g];
-        acc_s = fmaf(ev[g], y[E], acc_s);
+        const double* y = acr + (j + g) * A::kStride;
+        const double w = (double)ev[g];
+        S += w;
+        acc_s = fma(w, y[E], acc_s);
 #pragma unroll
-        for (int e = 0; e < E; ++e) acc_y[e] = fmaf(ev[g], y[e], acc_y[e]);
+        for (int e = 0; e < E; ++e) acc_y[e] = fma(w, y[e], acc_y[e]);
       }
     }
     __syncthreads();
     if (threadIdx.x == 0 && t + 2 < ntiles) issue(t + 2, sb);
   }
   if (!live) return;
-  // pi_ij = a_i 2^(lam f~_i) 2^(t_ij); sum_j 2^(t_ij) = 2^(-mq) S
-  const float scale = ex2(a.st->lam * a.f_tilde[i] + a.log2a[i] - mq);
+  // pi_ij = a_i 2^(lam f~_i) 2^(t_ij) and sum_j 2^(t_ij) = 2^(-mq) S
+  const double scale = exp2(a.st->lam_d * a.f_tilde[i] + a.log2a[i] - mq);
   a.row_mass[i] = S * scale;
   a.pi_s[i] = acc_s * scale;
 #pragma unroll
@@ -151,19 +147,19 @@ static __global__ void __launch_bounds__(128) plan_reduce_kernel(const PlanReduc
 constexpr int kRedThreads = 256;
 
 // Stage 1 of the outer-step row reduction: block b sums rows [b*rpb, (b+1)*rpb).
-static __global__ void outer_rows_kernel(const float* x, int64_t ldx, int d, const float* pi_y, int e,
-                                  int ld_piy, const float* r, const float* pi_s, const float* ft,
-                                  const float* s_half, const double* a, int64_t n, int64_t rpb,
-                                  double* part, int stride) {
+static __global__ void outer_rows_kernel(const double* x, int64_t ldx, int d, const double* pi_y,
+                                         int e, int ld_piy, const double* r, const double* pi_s,
+                                         const double* ft, const double* s_half, const double* a,
+                                         int64_t n, int64_t rpb, double* part, int stride) {
   __shared__ double red[32];
   const int64_t i0 = (int64_t)blockIdx.x * rpb, i1 = min(n, i0 + rpb);
   double v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0;
   for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     const double ri = r[i], si = s_half[i];
-    v0 += (double)ft[i] * ri;
+    v0 += ft[i] * ri;
     v1 += si * si * ri;
     v2 += fabs(ri - a[i]);
-    v3 += si * (double)pi_s[i];
+    v3 += si * pi_s[i];
     v4 += ri;
   }
   double* out = part + (int64_t)blockIdx.x * stride;
@@ -182,7 +178,7 @@ static __global__ void outer_rows_kernel(const float* x, int64_t ldx, int d, con
   for (int idx = threadIdx.x; idx < d * e; idx += blockDim.x) {
     const int p = idx / e, q = idx % e;
     double acc = 0.0;
-    for (int64_t i = i0; i < i1; ++i) acc += (double)x[i * ldx + p] * (double)pi_y[i * ld_piy + q];
+    for (int64_t i = i0; i < i1; ++i) acc += x[i * ldx + p] * pi_y[i * ld_piy + q];
     out[16 + idx] = acc;
   }
 }
@@ -197,16 +193,17 @@ static __global__ void sum_partials_kernel(const double* part, int nb, int strid
 }
 
 // Column side: c_j = b_j 2^(lam (g~_j - gt_j)) from the g-tentative of the final pair.
-static __global__ void outer_cols_kernel(const cntgw_sweep_state* st, const float* g, const float* gt,
-                                  const float* t_half, const double* b, int64_t m, double* part) {
+static __global__ void outer_cols_kernel(const cntgw_sweep_state* st, int prec, const double* g,
+                                         const double* gt, const double* t_half, const double* b,
+                                         int64_t m, double* part) {
   __shared__ double red[32];
-  const double lam = (double)st->lam;
+  const double lam = prec == CNTGW_F64 ? st->lam_d : (double)st->lam;
   double v0 = 0, v1 = 0, v2 = 0, v3 = 0;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m;
        j += (int64_t)gridDim.x * blockDim.x) {
-    const double c = b[j] * exp2(lam * ((double)g[j] - (double)gt[j]));
+    const double c = b[j] * exp2(lam * (g[j] - gt[j]));
     const double tj = t_half[j];
-    v0 += (double)g[j] * c;
+    v0 += g[j] * c;
     v1 += tj * tj * c;
     v2 += fabs(c - b[j]);
     v3 += c;
@@ -227,18 +224,20 @@ static __global__ void outer_cols_kernel(const cntgw_sweep_state* st, const floa
 }
 
 // out_i = op . feat_i  (op: dout x din fp64, staged in shared memory)
-static __global__ void apply_operator_kernel(const double* op, int dout, int din, const float* feat,
-                                      int64_t ld, int64_t n, float* out) {
+static __global__ void apply_operator_kernel(const double* op, int dout, int din, const double* feat,
+                                             int64_t ld, int64_t n, double* out64, float* out32,
+                                             int64_t ld_out) {
   extern __shared__ double sop[];
   for (int k = threadIdx.x; k < dout * din; k += blockDim.x) sop[k] = op[k];
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const float* fi = feat + i * ld;
+  const double* fi = feat + i * ld;
   for (int o = 0; o < dout; ++o) {
     double acc = 0.0;
-    for (int k = 0; k < din; ++k) acc += sop[o * din + k] * (double)fi[k];
-    out[i * dout + o] = (float)acc;
+    for (int k = 0; k < din; ++k) acc = fma(sop[o * din + k], fi[k], acc);
+    out64[i * ld_out + o] = acc;
+    if (out32) out32[i * ld_out + o] = (float)acc;
   }
 }
 

@@ -21,9 +21,10 @@ static __global__ void sweep_init_kernel(cntgw_sweep_state* st, double eps, doub
   st->eps_n = eps;
   st->gap_r = 0.0;
   st->gap_c = 0.0;
-  st->lam = (float)(kLog2eD / eps);
-  st->inv_lam = (float)(eps / kLog2eD);
-  st->sqrt_lam = (float)sqrt(kLog2eD / eps);
+  st->lam_d = kLog2eD / eps;
+  st->sqrt_lam_d = sqrt(st->lam_d);
+  st->lam = (float)st->lam_d;
+  st->sqrt_lam = (float)st->sqrt_lam_d;
   st->max_sweeps = max_sweeps;
   st->mode = mode;
   st->sweep = 0;
@@ -44,23 +45,25 @@ static __global__ void sweep_begin_kernel(cntgw_sweep_state* st) {
   double e = st->eps;
   if (st->anneal_from > 0.0) e = fmax(st->anneal_from / sqrt((double)k), st->eps);
   st->eps_n = e;
-  st->lam = (float)(kLog2eD / e);
-  st->inv_lam = (float)(e / kLog2eD);
-  st->sqrt_lam = (float)sqrt(kLog2eD / e);
+  st->lam_d = kLog2eD / e;
+  st->sqrt_lam_d = sqrt(st->lam_d);
+  st->lam = (float)st->lam_d;
+  st->sqrt_lam = (float)st->sqrt_lam_d;
   st->check = (st->threshold > 0.0) && (e == st->eps);  // sinkhorn.py:228
   st->sweep = k;
 }
 
 // sum_i w_i^2 |exp(min((pot_i - tent_i)/eps_n, 700)) - 1|  (sinkhorn.py:179-188)
-static __global__ void sweep_gap_kernel(const cntgw_sweep_state* st, const double* w, const float* pot,
-                                 const float* tent, int64_t n, double* partials) {
+static __global__ void sweep_gap_kernel(const cntgw_sweep_state* st, const double* w,
+                                        const double* pot, const double* tent, int64_t n,
+                                        double* partials) {
   __shared__ double red[32];
   if (st->done || !st->check) return;
   const double eps = st->eps_n;
   double acc = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const double r = fmin(((double)pot[i] - (double)tent[i]) / eps, 700.0);
+    const double r = fmin((pot[i] - tent[i]) / eps, 700.0);
     acc += w[i] * w[i] * fabs(exp(r) - 1.0);
   }
   const double t = block_sum_f64(acc, red);
@@ -94,12 +97,12 @@ static __global__ void sweep_finish_kernel(cntgw_sweep_state* st, const double* 
 }
 
 // symmetrized: pot <- (pot + tent)/2 (sinkhorn.py:238-239); standard: pot <- tent (:249)
-static __global__ void sweep_apply_kernel(const cntgw_sweep_state* st, float* pot, const float* tent,
-                                   int64_t n, int average) {
+static __global__ void sweep_apply_kernel(const cntgw_sweep_state* st, double* pot,
+                                          const double* tent, int64_t n, int average) {
   if (st->done) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    pot[i] = average ? 0.5f * (pot[i] + tent[i]) : tent[i];
+    pot[i] = average ? 0.5 * (pot[i] + tent[i]) : tent[i];
 }
 
 }  // namespace cntgw

@@ -1,29 +1,40 @@
-"""Device engine: the Sinkhorn loop and fused reductions on one GPU.
+"""Device engine: the Sinkhorn loop and its half-update operators on one GPU.
 
 Everything here operates on CUDA tensors and launches the C-ABI kernels of
 ``libcntgw_b200.so`` on torch's current stream. The loop state (sweep counter,
 eps_n, threshold decision, done flag) lives in device memory
 (``cntgw_sweep_state``), so sweeps are enqueued back to back without host
-round trips and chunks of sweeps can be replayed as CUDA graphs; the host
-reads the state once per chunk to learn whether a threshold run finished.
+round trips, and chunks of sweeps are replayed as CUDA graphs for small
+problems; the host reads the state once per chunk to learn whether a
+threshold run finished.
 
-Cost model every feature provider reduces to (see include/cntgw_b200.h):
+Cost model every feature provider reduces to (include/cntgw_b200.h):
     C_ij = row_sep_i + col_sep_j - 2 <xf_i, zf_j> + (xs_i - zs_j)^2
-with interaction potentials f~ = f - row_sep and g~ = g - col_sep on device.
+with fp64 interaction potentials f~ = f - row_sep, g~ = g - col_sep on device.
+
+Precision: the exponent t_ij is assembled in fp32 (FFMA2) when its terms are
+small enough that fp32 rounding stays below ~2e-4 log2 units, else in fp64
+(DFMA; B200 runs fp64 at half the fp32 rate). ``choose_precision`` makes the
+call from the problem's scales; CNTGW_PRECISION=f32|f64 forces it.
 """
 
 from __future__ import annotations
 
 import ctypes
+import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from . import _native
-from ._native import LIB, SweepStateStruct, call
+from ._native import F32, F64, LIB, SweepStateStruct, call
 
 SUPPORTED_KD = (1, 2, 3, 4, 8, 16, 32, 64)
+# fp32 exponent assembly is used while lam * (term magnitudes) stays below this
+# (fp32 ulp there is 2^-12 log2 units ~ 1.7e-4 relative error per plan entry)
+F32_EXPONENT_LIMIT = 4096.0
 
 
 def require_cuda(device=None) -> torch.device:
@@ -49,10 +60,13 @@ def _p(t) -> int:
     return 0 if t is None else t.data_ptr()
 
 
-def to_dev32(x, device, kd=None) -> torch.Tensor:
-    """float32 contiguous device copy, zero-padded to kd columns if given."""
-    t = torch.as_tensor(np.ascontiguousarray(x) if isinstance(x, np.ndarray) else x)
-    t = t.to(device=device, dtype=torch.float32)
+def to_dev(x, device, dtype, kd=None) -> torch.Tensor:
+    """Contiguous device copy in ``dtype``, zero-padded to kd columns if given."""
+    if isinstance(x, np.ndarray):
+        x = np.ascontiguousarray(x)
+        if not x.flags.writeable:
+            x = x.copy()
+    t = torch.as_tensor(x).to(device=device, dtype=dtype)
     if kd is not None:
         if t.ndim == 1:
             t = t[:, None]
@@ -61,9 +75,37 @@ def to_dev32(x, device, kd=None) -> torch.Tensor:
     return t.contiguous()
 
 
-def to_dev64(x, device) -> torch.Tensor:
-    t = torch.as_tensor(np.ascontiguousarray(x) if isinstance(x, np.ndarray) else x)
-    return t.to(device=device, dtype=torch.float64).contiguous()
+def to_dev64(x, device, kd=None) -> torch.Tensor:
+    return to_dev(x, device, torch.float64, kd)
+
+
+def to_dev32(x, device, kd=None) -> torch.Tensor:
+    return to_dev(x, device, torch.float32, kd)
+
+
+def exponent_scale(eps: float, feat_r, sq_r, feat_c, sq_c, pot_abs: float = 0.0) -> float:
+    """Upper bound (log2 units) of the terms the half-update adds: lam (|pot| +
+    2 |x||z| + (|s_r| + |s_c|)^2)."""
+    lam = math.log2(math.e) / eps
+
+    def rowmax(t):
+        return float(t.norm(dim=1).max()) if t.numel() else 0.0
+
+    def absmax(t):
+        return float(t.abs().max()) if t is not None and t.numel() else 0.0
+
+    dot = 2.0 * rowmax(feat_r) * rowmax(feat_c)
+    sq = (absmax(sq_r) + absmax(sq_c)) ** 2
+    return lam * (pot_abs + dot + sq)
+
+
+def choose_precision(scale: float) -> int:
+    forced = os.environ.get("CNTGW_PRECISION", "auto").lower()
+    if forced in ("f32", "fp32"):
+        return F32
+    if forced in ("f64", "fp64"):
+        return F64
+    return F32 if scale < F32_EXPONENT_LIMIT else F64
 
 
 class SweepState:
@@ -83,80 +125,107 @@ class SweepState:
         call("cntgw_sweep_begin", self.ptr, _stream())
 
     def read(self) -> SweepStateStruct:
-        host = self.buf.cpu().numpy().tobytes()
-        return SweepStateStruct.from_buffer_copy(host)
+        return SweepStateStruct.from_buffer_copy(self.buf.cpu().numpy().tobytes())
 
     def done_flag(self) -> bool:
         off = SweepStateStruct.done.offset
         return bool(self.buf[off:off + 4].cpu().view(torch.int32).item())
 
 
-@dataclass
 class Side:
-    """One marginal as the kernels see it (dot features, sq coordinate, weights)."""
+    """One marginal as the kernels see it: dot features (n x kd), the optional
+    squared-difference coordinate, weights. fp64 is the source of truth; the
+    fp32 copies feed the fp32 kernels."""
 
-    feat: torch.Tensor  # n x kd float32 (zero-padded)
-    sq: torch.Tensor | None  # n float32, the squared-difference coordinate
-    w: torch.Tensor  # n float64
-    log2w: torch.Tensor  # n float32
-
-    @property
-    def n(self) -> int:
-        return self.feat.shape[0]
-
-    @property
-    def kd(self) -> int:
-        return self.feat.shape[1]
+    def __init__(self, feat64: torch.Tensor, sq64: torch.Tensor | None, w: torch.Tensor):
+        self.feat64 = feat64
+        self.sq64 = sq64
+        self.w = w
+        self.log2w = torch.log2(w)
+        self._f32 = None
 
     @staticmethod
     def make(feat, sq, w, device, kd):
-        w64 = to_dev64(w, device)
-        return Side(
-            feat=to_dev32(feat, device, kd),
-            sq=None if sq is None else to_dev32(sq, device),
-            w=w64,
-            log2w=torch.log2(w64).to(torch.float32),
-        )
+        return Side(to_dev64(feat, device, kd), None if sq is None else to_dev64(sq, device),
+                    to_dev64(w, device))
+
+    @property
+    def n(self) -> int:
+        return self.feat64.shape[0]
+
+    @property
+    def kd(self) -> int:
+        return self.feat64.shape[1]
+
+    def refresh32(self):
+        """Re-round the fp32 copies in place (their addresses may be baked into
+        captured CUDA graphs, so they are never reallocated)."""
+        if self._f32 is None:
+            self._f32 = (self.feat64.float(), None if self.sq64 is None else self.sq64.float())
+        else:
+            self._f32[0].copy_(self.feat64)
+            if self.sq64 is not None:
+                self._f32[1].copy_(self.sq64)
+
+    def feat(self, prec):
+        if prec == F64:
+            return self.feat64, self.sq64
+        if self._f32 is None:
+            self.refresh32()
+        return self._f32
 
 
 class HalfUpdate:
     """out_rows = S(pot_cols): pack the column side's records, then stream them."""
 
-    def __init__(self, rows: Side, cols: Side, sq: bool):
+    def __init__(self, rows: Side, cols: Side, sq: bool, prec: int = F32):
         self.rows, self.cols, self.sq = rows, cols, bool(sq)
         self.kd = rows.kd
         assert cols.kd == self.kd
-        dev = rows.feat.device
-        stride = LIB.cntgw_col_stride(self.kd, int(self.sq))
-        _native.check(0 if stride > 0 else stride, "cntgw_col_stride")
-        self.stride = stride
-        self.rec = torch.empty(LIB.cntgw_cols_padded(cols.n) * stride, dtype=torch.float32, device=dev)
-        wsb = LIB.cntgw_softmin_workspace(rows.n, cols.n, self.kd, int(self.sq))
+        self.prec = prec
+        dev = rows.feat64.device
+        stride64 = LIB.cntgw_col_stride(F64, self.kd, int(self.sq))
+        _native.check(0 if stride64 > 0 else stride64, "cntgw_col_stride")
+        self.rec = torch.empty(LIB.cntgw_cols_padded(cols.n) * stride64, dtype=torch.float64, device=dev)
+        wsb = max(LIB.cntgw_softmin_workspace(p, rows.n, cols.n, self.kd, int(self.sq)) for p in (F32, F64))
         self.ws = torch.empty(max(int(wsb), 16), dtype=torch.uint8, device=dev)
 
-    def pack(self, state: SweepState, pot_cols: torch.Tensor | None):
+    def pack(self, state: SweepState, pot_cols: torch.Tensor | None, prec=None):
+        prec = self.prec if prec is None else prec
         c = self.cols
-        call("cntgw_prep_cols", state.ptr, self.kd, int(self.sq), c.feat.data_ptr(), self.kd,
-             _p(c.sq), _p(pot_cols), c.log2w.data_ptr(), c.n, self.rec.data_ptr(), _stream())
+        feat, sq = c.feat(prec)
+        call("cntgw_prep_cols", state.ptr, prec, self.kd, int(self.sq), feat.data_ptr(), self.kd,
+             _p(sq), _p(pot_cols), c.log2w.data_ptr(), c.n, self.rec.data_ptr(), _stream())
 
     def stream(self, state: SweepState, out=None, skip=True, row_add=None, out_max=None,
                out_sum=None):
         r = self.rows
-        call("cntgw_softmin", state.ptr, int(skip), self.kd, int(self.sq), r.feat.data_ptr(),
-             self.kd, _p(r.sq), _p(row_add), self.rec.data_ptr(), r.n, self.cols.n, _p(out),
-             _p(out_max), _p(out_sum), self.ws.data_ptr(), self.ws.numel(), _stream())
+        feat, sq = r.feat(self.prec)
+        call("cntgw_softmin", state.ptr, int(skip), self.prec, self.kd, int(self.sq),
+             feat.data_ptr(), self.kd, _p(sq), _p(row_add), self.rec.data_ptr(), r.n, self.cols.n,
+             _p(out), _p(out_max), _p(out_sum), self.ws.data_ptr(), self.ws.numel(), _stream())
 
     def __call__(self, state, pot_cols, out, skip=True, row_add=None):
         self.pack(state, pot_cols)
         self.stream(state, out, skip=skip, row_add=row_add)
 
+    def partials(self, state, pot_cols, out_max, out_sum, skip=True):
+        """Per-row partial LSE pairs (log2 units) over this operator's columns."""
+        self.pack(state, pot_cols)
+        self.stream(state, None, skip=skip, out_max=out_max, out_sum=out_sum)
+
+    def finalize(self, state, mx, sm, out, skip=True, row_add=None):
+        call("cntgw_lse_finalize", state.ptr, int(skip), self.prec, mx.data_ptr(), sm.data_ptr(),
+             _p(row_add), out.numel(), out.data_ptr(), _stream())
+
 
 class DenseHalfUpdate:
-    """Half-update over an explicit cost matrix (DenseCost provider)."""
+    """Half-update over an explicit fp32 cost matrix (DenseCost provider)."""
 
     def __init__(self, cost: torch.Tensor, cols_log2w: torch.Tensor):
         self.cost = cost.contiguous()
         self.log2w = cols_log2w
+        self.prec = F64
 
     def __call__(self, state, pot_cols, out, skip=True, row_add=None):
         n, m = self.cost.shape
@@ -201,22 +270,27 @@ class SinkhornLoop:
         self.a_w, self.b_w = a_w, b_w
         self.n, self.m = a_w.numel(), b_w.numel()
         self.state = SweepState(device)
-        self.ft = torch.zeros(self.n, dtype=torch.float32, device=device)
-        self.gt = torch.zeros(self.m, dtype=torch.float32, device=device)
+        self.ft = torch.zeros(self.n, dtype=torch.float64, device=device)
+        self.gt = torch.zeros(self.m, dtype=torch.float64, device=device)
         self.pr = torch.zeros(LIB.cntgw_gap_blocks(self.n), dtype=torch.float64, device=device)
         self.pc = torch.zeros(LIB.cntgw_gap_blocks(self.m), dtype=torch.float64, device=device)
         self._graphs = {}
 
-    # -- one sweep (all launches skip once the state says done) --------------
-    def _g_update(self, f, out):
-        if self.comm is None:
-            self.bwd(self.state, f, out)
-        else:
-            self.comm.g_update(self, f, out)
+    def set_precision(self, prec: int):
+        for op in (self.fwd, self.bwd):
+            if isinstance(op, HalfUpdate):
+                op.prec = prec
 
-    def _gap(self, side, w, pot, tent, partials):
-        call("cntgw_sweep_gap", self.state.ptr, side, w.data_ptr(), pot.data_ptr(),
-             tent.data_ptr(), pot.numel(), partials.data_ptr(), _stream())
+    # -- one sweep (every launch is a no-op once the state says done) --------
+    def _g_update(self, f, out, skip=True):
+        if self.comm is None:
+            self.bwd(self.state, f, out, skip=skip)
+        else:
+            self.comm.g_update(self, f, out, skip=skip)
+
+    def _gap(self, w, pot, tent, partials):
+        call("cntgw_sweep_gap", self.state.ptr, w.data_ptr(), pot.data_ptr(), tent.data_ptr(),
+             pot.numel(), partials.data_ptr(), _stream())
 
     def sweep(self, f, g, mode):
         st = self.state
@@ -224,8 +298,8 @@ class SinkhornLoop:
         if mode == "symmetrized":
             self.fwd(st, g, self.ft)
             self._g_update(f, self.gt)
-            self._gap(0, self.a_w, f, self.ft, self.pr)
-            self._gap(1, self.b_w, g, self.gt, self.pc)
+            self._gap(self.a_w, f, self.ft, self.pr)
+            self._gap(self.b_w, g, self.gt, self.pc)
             if self.comm is not None:
                 self.comm.reduce_gap_partials(self)
             call("cntgw_sweep_finish", st.ptr, self.pr.data_ptr(), self.n, self.pc.data_ptr(),
@@ -234,7 +308,7 @@ class SinkhornLoop:
             call("cntgw_sweep_apply", st.ptr, g.data_ptr(), self.gt.data_ptr(), self.m, 1, _stream())
         else:
             self.fwd(st, g, self.ft)
-            self._gap(0, self.a_w, f, self.ft, self.pr)
+            self._gap(self.a_w, f, self.ft, self.pr)
             if self.comm is not None:
                 self.comm.reduce_gap_partials(self)
             call("cntgw_sweep_finish", st.ptr, self.pr.data_ptr(), self.n, 0, 0, _stream())
@@ -242,7 +316,7 @@ class SinkhornLoop:
             self._g_update(f, g)
 
     def run(self, f, g, cfg: LoopConfig, chunk: int | None = None, use_graph: bool = False) -> LoopStats:
-        """Run the loop to completion; f, g (interaction potentials) are updated in place."""
+        """Run the loop to completion; f, g (fp64 interaction potentials) update in place."""
         self.state.init(cfg.eps, cfg.anneal_from, cfg.threshold, cfg.max_sweeps, cfg.mode)
         total = cfg.max_sweeps
         if chunk is None:
@@ -258,18 +332,17 @@ class SinkhornLoop:
             launched += k
             if cfg.threshold is not None and launched < total and self.state.done_flag():
                 break
-        # one more begin() marks a fully used budget as done
-        self.state.begin()
+        self.state.begin()  # marks a fully used budget as done
         s = self.state.read()
         broke = bool(s.converged) and cfg.threshold is not None
         return LoopStats(iterations=int(s.applied), converged=bool(s.converged),
-                         eps_eff=float(s.eps_n), broke=broke, lam=float(s.lam))
+                         eps_eff=float(s.eps_n), broke=broke, lam=float(s.lam_d))
 
     def _replay(self, f, g, mode, k):
-        key = (f.data_ptr(), g.data_ptr(), mode, k)
+        prec = tuple(getattr(op, "prec", None) for op in (self.fwd, self.bwd))
+        key = (f.data_ptr(), g.data_ptr(), mode, k, prec)
         graph = self._graphs.get(key)
         if graph is None:
-            # warm-up launch outside capture sets kernel attributes once
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())
             graph = torch.cuda.CUDAGraph()
@@ -278,7 +351,6 @@ class SinkhornLoop:
                     self.sweep(f, g, mode)
             torch.cuda.current_stream().wait_stream(side)
             self._graphs[key] = graph
-            # the capture did not execute anything: fall through to replay
         graph.replay()
 
     def tentatives(self, f, g, need_f=True, need_g=True):
@@ -286,17 +358,13 @@ class SinkhornLoop:
         if need_f:
             self.fwd(self.state, g, self.ft, skip=False)
         if need_g:
-            if self.comm is None:
-                self.bwd(self.state, f, self.gt, skip=False)
-            else:
-                self.comm.g_update(self, f, self.gt, skip=False)
+            self._g_update(f, self.gt, skip=False)
         return self.ft, self.gt
 
     def marginal_error(self, f, g, lam):
         """Unweighted L1 error ||r - a||_1 + ||c - b||_1 from the tentatives (fp64)."""
-        lam = float(lam)
-        r = self.a_w * torch.exp2(lam * (f.double() - self.ft.double()))
-        c = self.b_w * torch.exp2(lam * (g.double() - self.gt.double()))
+        r = self.a_w * torch.exp2(lam * (f - self.ft))
+        c = self.b_w * torch.exp2(lam * (g - self.gt))
         err_r = (r - self.a_w).abs().sum()
         if self.comm is not None:
             err_r = self.comm.all_sum(err_r)

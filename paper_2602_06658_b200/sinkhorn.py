@@ -218,6 +218,20 @@ def feature_problem(row_feat, row_sq, col_feat, col_sq, a, b, device) -> tuple:
     return src, tgt, engine.HalfUpdate(src, tgt, sq), engine.HalfUpdate(tgt, src, sq)
 
 
+def _set_precision(problem, eps, f0, g0):
+    """Pick fp32/fp64 exponent assembly from the problem's scales (engine.py)."""
+    fwd = problem.fwd
+    if not isinstance(fwd, engine.HalfUpdate):
+        return
+    pot = max(float(np.abs(f0 - problem.row_sep).max(initial=0.0)),
+              float(np.abs(g0 - problem.col_sep).max(initial=0.0)))
+    scale = engine.exponent_scale(eps, fwd.rows.feat64, fwd.rows.sq64, fwd.cols.feat64,
+                                  fwd.cols.sq64, pot)
+    prec = engine.choose_precision(scale)
+    problem.fwd.prec = prec
+    problem.bwd.prec = prec
+
+
 def device_problem(cost, a, b, device) -> DeviceProblem:
     if isinstance(cost, SquaredEuclideanCost):
         x, z = cost._x, cost._z
@@ -237,8 +251,8 @@ def device_problem(cost, a, b, device) -> DeviceProblem:
         )
     dense = cost.full() if hasattr(cost, "full") else cost.rows(0, n)
     c = torch.as_tensor(np.ascontiguousarray(dense), dtype=torch.float32, device=device)
-    la = torch.log2(engine.to_dev64(a, device)).float()
-    lb = torch.log2(engine.to_dev64(b, device)).float()
+    la = torch.log2(engine.to_dev64(a, device))
+    lb = torch.log2(engine.to_dev64(b, device))
     fwd = engine.DenseHalfUpdate(c, lb)
     bwd = engine.DenseHalfUpdate(c.t().contiguous(), la)
     return DeviceProblem(fwd, bwd, np.zeros(n), np.zeros(m))
@@ -248,8 +262,11 @@ def run_loop(problem: DeviceProblem, a, b, config: SinkhornConfig, f0, g0, devic
     """Run the device loop from reference-parametrised (f0, g0); returns the
     reference-parametrised potentials, stats and the marginal error."""
     a_w, b_w = engine.to_dev64(a, device), engine.to_dev64(b, device)
-    ft = engine.to_dev32(np.asarray(f0, dtype=np.float64) - problem.row_sep, device)
-    gt = engine.to_dev32(np.asarray(g0, dtype=np.float64) - problem.col_sep, device)
+    f0 = np.asarray(f0, dtype=np.float64)
+    g0 = np.asarray(g0, dtype=np.float64)
+    _set_precision(problem, min(config.eps, config.anneal_from or config.eps), f0, g0)
+    ft = engine.to_dev64(f0 - problem.row_sep, device)
+    gt = engine.to_dev64(g0 - problem.col_sep, device)
     loop = engine.SinkhornLoop(problem.fwd, problem.bwd, a_w, b_w, device)
     cfg = config.loop_config()
     small = a_w.numel() * b_w.numel() <= _GRAPH_MAX_PAIRS
@@ -257,8 +274,8 @@ def run_loop(problem: DeviceProblem, a, b, config: SinkhornConfig, f0, g0, devic
     sym_break = stats.broke and cfg.mode == "symmetrized"
     loop.tentatives(ft, gt, need_f=not stats.broke, need_g=not sym_break)
     err = loop.marginal_error(ft, gt, stats.lam)
-    f = ft.double().cpu().numpy() + problem.row_sep
-    g = gt.double().cpu().numpy() + problem.col_sep
+    f = ft.cpu().numpy() + problem.row_sep
+    g = gt.cpu().numpy() + problem.col_sep
     return f, g, stats, err, (ft, gt, loop)
 
 

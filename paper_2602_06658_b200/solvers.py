@@ -31,7 +31,7 @@ import numpy as np
 import torch
 
 from . import divergence, engine
-from ._native import LIB, call
+from ._native import F32, F64, LIB, call
 from .measures import DenseCoupling, ImplicitCoupling
 from .sinkhorn import SinkhornConfig, SquaredEuclideanCost, sinkhorn
 
@@ -174,45 +174,38 @@ class _GwDevice:
         y = np.asarray(tgt.features, dtype=np.float64)
         self.n, self.d = x.shape
         self.m, self.e = y.shape
-        self.x = engine.to_dev32(x, device)
-        self.y = engine.to_dev32(y, device)
-        self.x64 = engine.to_dev64(x, device)
-        self.y64 = engine.to_dev64(y, device)
-        self.sx = engine.to_dev32(_half_sq(src), device)
-        self.ty = engine.to_dev32(_half_sq(tgt), device)
-        self.sx64 = engine.to_dev64(_half_sq(src), device)
-        self.ty64 = engine.to_dev64(_half_sq(tgt), device)
+        self.x = engine.to_dev64(x, device)
+        self.y = engine.to_dev64(y, device)
+        self.sx = engine.to_dev64(_half_sq(src), device)
+        self.ty = engine.to_dev64(_half_sq(tgt), device)
         self.a = engine.to_dev64(src.weights, device)
         self.b = engine.to_dev64(tgt.weights, device)
         self.proj_rows = self.d > self.e  # E-side projection
         self.k = min(self.d, self.e)
         self.kd = engine.padded_kd(self.k)
         if self.proj_rows:
-            rows_feat = torch.zeros(self.n, self.kd, dtype=torch.float32, device=device)
-            cols_feat = engine.to_dev32(y, device, self.kd)
+            rows_feat = torch.zeros(self.n, self.kd, dtype=torch.float64, device=device)
+            cols_feat = engine.to_dev64(y, device, self.kd)
         else:
-            rows_feat = engine.to_dev32(x, device, self.kd)
-            cols_feat = torch.zeros(self.m, self.kd, dtype=torch.float32, device=device)
-        log2a = torch.log2(self.a).float()
-        log2b = torch.log2(self.b).float()
-        self.src = engine.Side(rows_feat, self.sx, self.a, log2a)
-        self.tgt = engine.Side(cols_feat, self.ty, self.b, log2b)
+            rows_feat = engine.to_dev64(x, device, self.kd)
+            cols_feat = torch.zeros(self.m, self.kd, dtype=torch.float64, device=device)
+        self.src = engine.Side(rows_feat, self.sx, self.a)
+        self.tgt = engine.Side(cols_feat, self.ty, self.b)
         self.fwd = engine.HalfUpdate(self.src, self.tgt, True)
         self.bwd = engine.HalfUpdate(self.tgt, self.src, True)
         self.loop = engine.SinkhornLoop(self.fwd, self.bwd, self.a, self.b, device)
-        self.proj_tmp = torch.empty(max(self.n, self.m) * self.k, dtype=torch.float32, device=device)
         # K4 / K7 buffers
-        self.r = torch.empty(self.n, dtype=torch.float32, device=device)
-        self.pi_y = torch.empty(self.n * self.e, dtype=torch.float32, device=device)
-        self.pi_s = torch.empty(self.n, dtype=torch.float32, device=device)
+        self.r = torch.empty(self.n, dtype=torch.float64, device=device)
+        self.pi_y = torch.empty(self.n * self.e, dtype=torch.float64, device=device)
+        self.pi_s = torch.empty(self.n, dtype=torch.float64, device=device)
         self.argmax = torch.empty(self.n, dtype=torch.int64, device=device)
-        self.ws_plan = torch.empty(int(LIB.cntgw_plan_reduce_workspace(self.n, self.m, self.kd, 1, self.e)),
+        self.ws_plan = torch.empty(int(LIB.cntgw_plan_reduce_workspace(self.n, self.m, self.kd, self.e)),
                                    dtype=torch.uint8, device=device)
         self.acc = torch.zeros(16 + self.d * self.e + 8, dtype=torch.float64, device=device)
         ows = max(int(LIB.cntgw_outer_reduce_workspace(self.n, self.d, self.e)),
                   int(LIB.cntgw_outer_reduce_workspace(self.m, 1, 1)))
         self.ws_outer = torch.empty(ows, dtype=torch.uint8, device=device)
-        self.gamma_dev = torch.zeros(self.d * self.e, dtype=torch.float64, device=device)
+        self.prec = F32
 
     # -- K5 -----------------------------------------------------------------
     def set_gamma(self, gamma: np.ndarray):
@@ -222,35 +215,37 @@ class _GwDevice:
         else:  # cols: Gamma Y_j  (op = Gamma, D x E)
             op, side, feat, count, din, dout = g.contiguous(), self.tgt, self.y, self.m, self.e, self.d
         self._op = op  # keep alive until the launch completes
-        if dout == self.kd:
-            out = side.feat
-        else:
-            out = self.proj_tmp[: count * dout]
         call("cntgw_apply_operator", op.data_ptr(), dout, din, feat.data_ptr(), din, count,
-             out.data_ptr(), _stream())
-        if dout != self.kd:
-            side.feat[:, :dout].copy_(out.view(count, dout))
+             side.feat64.data_ptr(), 0, self.kd, _stream())
+        side.refresh32()
 
     def col_sep(self, gamma) -> torch.Tensor:
         """|Gamma Y_j|^2 in fp64 (reference separable column part)."""
         g = torch.as_tensor(np.ascontiguousarray(gamma, dtype=np.float64), device=self.device)
-        return ((self.y64 @ g.t()) ** 2).sum(1)
+        return ((self.y @ g.t()) ** 2).sum(1)
 
     def row_sep(self) -> torch.Tensor:
-        return (self.x64 ** 2).sum(1)
+        return (self.x ** 2).sum(1)
+
+    def choose_precision(self, f, g, eps_min):
+        pot = float(torch.maximum(f.abs().max(), g.abs().max()))
+        scale = engine.exponent_scale(eps_min, self.src.feat64, self.sx, self.tgt.feat64, self.ty, pot)
+        self.prec = engine.choose_precision(scale)
+        self.loop.set_precision(self.prec)
 
     # -- one outer step ------------------------------------------------------
     def step(self, f, g, gamma: np.ndarray, loop_cfg: engine.LoopConfig, eps_outer: float,
              const: float, use_graph: bool):
         self.set_gamma(gamma)
+        self.choose_precision(f, g, loop_cfg.eps)
         stats = self.loop.run(f, g, loop_cfg, use_graph=use_graph)
         sym_break = stats.broke and loop_cfg.mode == "symmetrized"
         if not sym_break:
             self.loop.tentatives(f, g, need_f=False, need_g=True)
         st = self.loop.state
-        self.fwd.pack(st, g)  # target records at the final lambda for the plan pass
+        self.fwd.pack(st, g, prec=F64)  # fp64 target records at the final lambda for K4
         stream = _stream()
-        call("cntgw_plan_reduce", st.ptr, self.kd, 1, self.e, self.src.feat.data_ptr(), self.kd,
+        call("cntgw_plan_reduce", st.ptr, self.kd, self.e, self.src.feat64.data_ptr(), self.kd,
              self.sx.data_ptr(), f.data_ptr(), self.src.log2w.data_ptr(), self.fwd.rec.data_ptr(),
              self.y.data_ptr(), self.e, self.ty.data_ptr(), self.n, self.m, self.r.data_ptr(),
              self.pi_y.data_ptr(), self.pi_s.data_ptr(), self.argmax.data_ptr(),
@@ -326,15 +321,15 @@ class _CntGwState:
         self.gamma = _initial_gamma(src, tgt, cfg)
         if warm_potentials is None:
             # interaction potentials 0 (solvers.py:297-301): f~ = s^2, g~ = t^2
-            self.f = (self.dev.sx64 ** 2).float()
-            self.g = (self.dev.ty64 ** 2).float()
+            self.f = self.dev.sx ** 2
+            self.g = self.dev.ty ** 2
         else:
             f0 = engine.to_dev64(np.asarray(warm_potentials[0], dtype=np.float64), self.device)
             g0 = engine.to_dev64(np.asarray(warm_potentials[1], dtype=np.float64), self.device)
-            self.f = (f0 - self.dev.row_sep()).float()
-            self.g = (g0 - self.dev.col_sep(self.gamma)).float()
-        mx = divergence.moments(self.dev.x64, self.dev.a, self.device).cpu().numpy()
-        my = divergence.moments(self.dev.y64, self.dev.b, self.device).cpu().numpy()
+            self.f = f0 - self.dev.row_sep()
+            self.g = g0 - self.dev.col_sep(self.gamma)
+        mx = divergence.moments(self.dev.x, self.dev.a, self.device).cpu().numpy()
+        my = divergence.moments(self.dev.y, self.dev.b, self.device).cpu().numpy()
         self.constant = divergence.constant_from_moments(mx, self.dev.d, my, self.dev.e)
         self.coupling_gamma = None
         self.eps_eff = None
@@ -362,8 +357,8 @@ class _CntGwState:
         """The last plan (built on Gamma_t, solvers.py:326-336) in reference form."""
         dev = self.dev
         gt = self.coupling_gamma
-        f = (self.f.double() + dev.row_sep()).cpu().numpy()
-        g = (self.g.double() + dev.col_sep(gt)).cpu().numpy()
+        f = (self.f + dev.row_sep()).cpu().numpy()
+        g = (self.g + dev.col_sep(gt)).cpu().numpy()
         src, tgt = self.src, self.tgt
         xbar = np.column_stack([src.features, _half_sq(src)])
         zbar = np.column_stack([np.asarray(tgt.features) @ gt.T, _half_sq(tgt)])
@@ -471,22 +466,22 @@ def _plan_pass(coupling, src, tgt):
     e = np.asarray(tgt.features).shape[1]
     from .sinkhorn import feature_problem
 
-    srcs, tgts, fwd, _ = feature_problem(xf, x[:, -1], zf, z[:, -1], coupling.source_weights,
-                                         coupling.target_weights, dev)
-    f = engine.to_dev32(coupling.f - (xf * xf).sum(1), dev)
-    g = engine.to_dev32(coupling.g - (zf * zf).sum(1), dev)
+    srcs, _, fwd, _ = feature_problem(xf, x[:, -1], zf, z[:, -1], coupling.source_weights,
+                                      coupling.target_weights, dev)
+    f = engine.to_dev64(coupling.f - (xf * xf).sum(1), dev)
+    g = engine.to_dev64(coupling.g - (zf * zf).sum(1), dev)
     st = engine.SweepState(dev)
     st.init(coupling.eps_eff)
-    fwd.pack(st, g)
+    fwd.pack(st, g, prec=F64)
     n, m = cost.shape
-    r = torch.empty(n, dtype=torch.float32, device=dev)
-    pi_y = torch.empty(n * e, dtype=torch.float32, device=dev)
-    pi_s = torch.empty(n, dtype=torch.float32, device=dev)
+    r = torch.empty(n, dtype=torch.float64, device=dev)
+    pi_y = torch.empty(n * e, dtype=torch.float64, device=dev)
+    pi_s = torch.empty(n, dtype=torch.float64, device=dev)
     am = torch.empty(n, dtype=torch.int64, device=dev)
-    ws = torch.empty(int(LIB.cntgw_plan_reduce_workspace(n, m, kd, 1, e)), dtype=torch.uint8, device=dev)
-    y = engine.to_dev32(tgt.features, dev)
-    ty = engine.to_dev32(_half_sq(tgt), dev)
-    call("cntgw_plan_reduce", st.ptr, kd, 1, e, srcs.feat.data_ptr(), kd, srcs.sq.data_ptr(),
+    ws = torch.empty(int(LIB.cntgw_plan_reduce_workspace(n, m, kd, e)), dtype=torch.uint8, device=dev)
+    y = engine.to_dev64(tgt.features, dev)
+    ty = engine.to_dev64(_half_sq(tgt), dev)
+    call("cntgw_plan_reduce", st.ptr, kd, e, srcs.feat64.data_ptr(), kd, srcs.sq64.data_ptr(),
          f.data_ptr(), srcs.log2w.data_ptr(), fwd.rec.data_ptr(), y.data_ptr(), e, ty.data_ptr(),
          n, m, r.data_ptr(), pi_y.data_ptr(), pi_s.data_ptr(), am.data_ptr(), ws.data_ptr(),
          ws.numel(), _stream())
@@ -502,7 +497,7 @@ def gamma_step(coupling, src, tgt) -> np.ndarray:
         return (xt.t() @ (pi @ torch.as_tensor(np.asarray(tgt.features), device=dev))).cpu().numpy()
     _, pi_y, _, _ = _plan_pass(coupling, src, tgt)
     x = torch.as_tensor(np.asarray(src.features), device=pi_y.device)
-    return (x.t() @ pi_y.double()).cpu().numpy()
+    return (x.t() @ pi_y).cpu().numpy()
 
 
 def egw_objective(gamma, coupling, src, tgt, eps: float) -> float:
@@ -513,8 +508,8 @@ def egw_objective(gamma, coupling, src, tgt, eps: float) -> float:
     if isinstance(coupling, ImplicitCoupling):
         r, pi_y, pi_s, _ = _plan_pass(coupling, src, tgt)
         x = torch.as_tensor(np.asarray(src.features), device=pi_y.device)
-        xt_pi_y = (x.t() @ pi_y.double()).cpu().numpy()
-        sigma_ss = float((torch.as_tensor(_half_sq(src), device=pi_y.device) * pi_s.double()).sum())
+        xt_pi_y = (x.t() @ pi_y).cpu().numpy()
+        sigma_ss = float((torch.as_tensor(_half_sq(src), device=pi_y.device) * pi_s).sum())
         kl = kl_divergence(coupling)
     else:
         pi = coupling.matrix

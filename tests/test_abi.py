@@ -37,28 +37,30 @@ def test_library_exports_every_declared_symbol():
 def test_abi_version_and_state_layout():
     from paper_2602_06658_b200 import _native
 
-    assert _native.LIB.cntgw_abi_version() == 1
+    assert _native.LIB.cntgw_abi_version() == 2
     assert _native.LIB.cntgw_sweep_state_size() == ctypes.sizeof(_native.SweepStateStruct)
 
 
-@pytest.mark.parametrize("kd,sq,stride", [(1, 0, 4), (3, 1, 8), (4, 0, 8), (16, 0, 20), (32, 1, 36),
-                                          (64, 1, 68)])
-def test_column_record_stride(kd, sq, stride):
+@pytest.mark.parametrize("prec,kd,sq,stride", [
+    (0, 1, 0, 4), (0, 3, 1, 8), (0, 4, 0, 8), (0, 16, 0, 20), (0, 32, 1, 36), (0, 64, 1, 68),
+    (1, 1, 0, 2), (1, 3, 1, 6), (1, 4, 0, 6), (1, 16, 0, 18), (1, 32, 1, 34), (1, 64, 1, 66)])
+def test_column_record_stride(prec, kd, sq, stride):
     from paper_2602_06658_b200 import _native
 
-    assert _native.LIB.cntgw_col_stride(kd, sq) == stride
+    assert _native.LIB.cntgw_col_stride(prec, kd, sq) == stride
 
 
 def test_invalid_arguments_report_errors_without_gpu():
     from paper_2602_06658_b200 import _native
 
-    assert _native.LIB.cntgw_col_stride(5, 0) == -1
+    assert _native.LIB.cntgw_col_stride(0, 5, 0) == -1
     assert b"kd=5" in _native.LIB.cntgw_last_error()
-    rc = _native.LIB.cntgw_softmin(None, 0, 3, 1, None, 3, None, None, None, 0, 0, None, None,
+    assert _native.LIB.cntgw_col_stride(7, 4, 0) == -1
+    rc = _native.LIB.cntgw_softmin(None, 0, 0, 3, 1, None, 3, None, None, None, 0, 0, None, None,
                                    None, None, 0, None)
     assert rc == -1 and b"softmin" in _native.LIB.cntgw_last_error()
     with pytest.raises(_native.NativeError, match="prep_cols"):
-        _native.call("cntgw_prep_cols", None, 3, 1, None, 3, None, None, None, 0, None, None)
+        _native.call("cntgw_prep_cols", None, 0, 3, 1, None, 3, None, None, None, 0, None, None)
 
 
 def test_padding_helpers():

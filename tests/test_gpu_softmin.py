@@ -36,21 +36,24 @@ def env(cuda):
     return P, engine, S, O, torch, cuda
 
 
-def _half_update(env, cost, a, b, g, eps):
+def _half_update(env, cost, a, b, g, eps, prec=None):
     """GPU f-update S(g) through the device problem of ``cost`` (reference form)."""
     P, engine, S, O, torch, dev = env
     prob = S.device_problem(cost, a, b, dev)
+    if prec is not None:
+        prob.fwd.prec = prec
     st = engine.SweepState(dev)
     st.init(eps)
-    gt = engine.to_dev32(np.asarray(g) - prob.col_sep, dev)
-    out = torch.empty(len(a), dtype=torch.float32, device=dev)
+    gt = engine.to_dev64(np.asarray(g) - prob.col_sep, dev)
+    out = torch.empty(len(a), dtype=torch.float64, device=dev)
     prob.fwd(st, gt, out, skip=False)
-    return out.double().cpu().numpy() + prob.row_sep
+    return out.cpu().numpy() + prob.row_sep
 
 
+@pytest.mark.parametrize("prec", [0, 1], ids=["f32", "f64"])
 @pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 8, 16, 17, 33, 64, 65])
 @pytest.mark.parametrize("n,m", [(1, 1), (1, 300), (300, 1), (129, 257), (1000, 1000), (2049, 771)])
-def test_sq_euclidean_half_update(env, k, n, m):
+def test_sq_euclidean_half_update(env, k, n, m, prec):
     P, engine, S, O, torch, dev = env
     rng = np.random.default_rng(k * 1000 + n + m)
     x = rng.standard_normal((n, k)) * 0.5
@@ -61,9 +64,9 @@ def test_sq_euclidean_half_update(env, k, n, m):
     b /= b.sum()
     g = rng.standard_normal(m) * 0.1 + (z * z).sum(1)
     eps = 0.05
-    got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps)
+    got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, prec)
     want = O.softmin(O.SqEuclid(x, z), np.log(b), g, eps)
-    assert _rel(got, want) < 1e-5
+    assert _rel(got, want) < (1e-5 if prec == 0 else 1e-7)
 
 
 @pytest.mark.parametrize("k", [4, 16])
@@ -79,7 +82,8 @@ def test_low_rank_half_update(env, k):
     assert _rel(got, want) < 1e-5
 
 
-def test_rebase_path_under_huge_exponents(env):
+@pytest.mark.parametrize("prec", [0, 1], ids=["f32", "f64"])
+def test_rebase_path_under_huge_exponents(env, prec):
     """Cold regime: |exponent| ~ 1e6 log2 units; exercises lazy rebasing."""
     P, engine, S, O, torch, dev = env
     rng = np.random.default_rng(0)
@@ -88,9 +92,9 @@ def test_rebase_path_under_huge_exponents(env):
     a, b = np.full(700, 1 / 700), np.full(900, 1 / 900)
     g = rng.standard_normal(900) * 30.0 + (z * z).sum(1)
     eps = 1.25e-3
-    got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps)
+    got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, prec)
     want = O.softmin(O.SqEuclid(x, z), np.log(b), g, eps)
-    assert _rel(got, want) < 1e-5
+    assert _rel(got, want) < (1e-5 if prec == 0 else 1e-7)
 
 
 def test_deterministic_reruns(env):

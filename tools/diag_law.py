@@ -40,8 +40,8 @@ def main(name, eps, n_inner, steps=10):
             f_ref = engine.to_dev64(g["f_steps"][k - 1], dev.device)
             g_ref = engine.to_dev64(g["g_steps"][k - 1], dev.device)
             st2.gamma = gamma_cur
-            st2.f.copy_((f_ref - st2.dev.row_sep()).float())
-            st2.g.copy_((g_ref - st2.dev.col_sep(gamma_prev)).float())
+            st2.f.copy_(f_ref - st2.dev.row_sep())
+            st2.g.copy_(g_ref - st2.dev.col_sep(gamma_prev))
         s = st2.step()
         cp = st2.coupling()
         print(f"  {k + 1:2d} {rel(cp.f, g['f_steps'][k]):.2e} {rel(cp.g, g['g_steps'][k]):.2e} "
