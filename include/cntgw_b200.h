@@ -52,7 +52,9 @@ typedef enum cntgw_status {
   CNTGW_ENOSPACE = -3  /* workspace smaller than the *_workspace query */
 } cntgw_status;
 
-typedef enum cntgw_precision { CNTGW_F32 = 0, CNTGW_F64 = 1 } cntgw_precision;
+/* Exponent assembly: fp32 FFMA2, fp64 DFMA, or the tcgen05 tensor cores with a
+ * 3xTF32 split (kd in {8, 16}, no sq coordinate; well-scaled problems). */
+typedef enum cntgw_precision { CNTGW_F32 = 0, CNTGW_F64 = 1, CNTGW_TF32X3 = 2 } cntgw_precision;
 
 /* Device-resident state of one Sinkhorn loop (sinkhorn.py:191-258 control).
  * Lives in device memory; the host initialises it with cntgw_sweep_init and

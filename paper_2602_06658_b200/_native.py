@@ -32,7 +32,7 @@ class SweepStateStruct(ctypes.Structure):
     ]
 
 
-F32, F64 = 0, 1  # cntgw_precision
+F32, F64, TF32X3 = 0, 1, 2  # cntgw_precision
 
 # name -> (restype, argtypes); every symbol include/cntgw_b200.h declares
 SIGNATURES = {

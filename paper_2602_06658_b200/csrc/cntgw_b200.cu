@@ -7,6 +7,7 @@
 
 #include "common.cuh"
 #include "softmin.cuh"
+#include "softmin_tc.cuh"
 #include "sweep.cuh"
 
 using namespace cntgw;
@@ -77,8 +78,9 @@ constexpr int stage_cols() {
 
 struct KernelPick {
   void* fn;
-  int rows;  // rows per thread
+  int rows;  // rows per thread (CTA rows = 128 * rows)
   size_t smem;
+  int threads = 128;
 };
 
 template <int PREC, int KD, int SQ>
@@ -103,7 +105,24 @@ KernelPick pick() {
   X(PREC, 4, 0) X(PREC, 4, 1) X(PREC, 8, 0) X(PREC, 8, 1) X(PREC, 16, 0) X(PREC, 16, 1) \
   X(PREC, 32, 0) X(PREC, 32, 1) X(PREC, 64, 0) X(PREC, 64, 1)
 
+template <int KD>
+KernelPick pick_tc() {
+  using L = TcLayout<KD>;
+  KernelPick k;
+  k.fn = (void*)softmin_tc_kernel<KD>;
+  k.rows = 1;  // 128 rows per CTA = 128 threads x 1 in the planner's units
+  k.smem = (size_t)(L::kATileFloats + 2 * L::kBTileFloats) * sizeof(float);
+  k.threads = kTcThreads;
+  return k;
+}
+
 bool lookup(int prec, int kd, int sq, KernelPick* out) {
+  if (prec == CNTGW_TF32X3) {
+    if (sq) return false;
+    if (kd == 8) { *out = pick_tc<8>(); return true; }
+    if (kd == 16) { *out = pick_tc<16>(); return true; }
+    return false;
+  }
 #define PICK_CASE(P, K, Q) \
   if (prec == P && kd == K && (sq ? 1 : 0) == Q) { *out = pick<P, K, Q>(); return true; }
   KD_SQ_CASES(CNTGW_F32, PICK_CASE)
@@ -126,7 +145,7 @@ Plan plan_softmin(int64_t n, int64_t m, const KernelPick& k) {
   p.row_tiles = (int)((n + rows_per_cta - 1) / rows_per_cta);
   const int64_t tiles = (m + kColTile - 1) / kColTile;
   int occ = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, 128, k.smem) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, k.threads, k.smem) != cudaSuccess) {
     cudaGetLastError();
     occ = 1;
   }
@@ -227,6 +246,11 @@ int cntgw_col_stride(int prec, int kd, int sq) {
   const int raw = kd + (sq ? 1 : 0) + 1;
   if (prec == CNTGW_F32) return (raw + 3) / 4 * 4;
   if (prec == CNTGW_F64) return (raw + 1) / 2 * 2;
+  if (prec == CNTGW_TF32X3) {
+    if (sq || (kd != 8 && kd != 16))
+      return fail(CNTGW_EINVAL, "tensor-core path supports kd in {8,16} without sq (kd=%d sq=%d)", kd, sq);
+    return (3 * kd + 2 + 7) / 8 * 8;  // K' floats per column, in 256-column tiles
+  }
   return fail(CNTGW_EINVAL, "unknown precision %d", prec);
 }
 int64_t cntgw_cols_padded(int64_t m) { return (m + kColTile - 1) / kColTile * kColTile; }
@@ -284,6 +308,15 @@ int cntgw_prep_cols(const cntgw_sweep_state* st, int prec, int kd, int sq_flag, 
   const int th = 256;
   const unsigned blocks = (unsigned)((mpad + th - 1) / th);
   const int sqf = sq_flag ? 1 : 0;
+  if (prec == CNTGW_TF32X3) {
+    if (kd == 8)
+      prep_cols_tc_kernel<8><<<blocks, th, 0, as_stream(stream)>>>(
+          st, static_cast<const float*>(feat), ld, pot, log2w, m, mpad, static_cast<float*>(rec));
+    else
+      prep_cols_tc_kernel<16><<<blocks, th, 0, as_stream(stream)>>>(
+          st, static_cast<const float*>(feat), ld, pot, log2w, m, mpad, static_cast<float*>(rec));
+    return check_launch("prep_cols_tc");
+  }
   if (prec == CNTGW_F32)
     prep_cols_kernel<float><<<blocks, th, 0, as_stream(stream)>>>(
         st, kd, sqf, stride, static_cast<const float*>(feat), ld, static_cast<const float*>(sq), pot,
@@ -312,8 +345,8 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
   KernelPick k;
   if (!lookup(prec, kd, sq_flag, &k))
     return fail(CNTGW_EINVAL, "softmin: unsupported precision %d / feature width kd=%d", prec, kd);
-  static bool attr_done[2][65][2] = {};
-  bool& done = attr_done[prec & 1][kd][sq_flag ? 1 : 0];
+  static bool attr_done[3][65][2] = {};
+  bool& done = attr_done[prec % 3][kd][sq_flag ? 1 : 0];
   if (!done) {
     cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem);
     done = true;
@@ -344,7 +377,7 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
   cudaStream_t s = as_stream(stream);
   void* args[] = {&a};
   const cudaError_t e =
-      cudaLaunchKernel(k.fn, dim3(p.row_tiles, p.nchunks), dim3(128), args, k.smem, s);
+      cudaLaunchKernel(k.fn, dim3(p.row_tiles, p.nchunks), dim3(k.threads), args, k.smem, s);
   if (e != cudaSuccess) {
     cudaGetLastError();  // clear, so the failure is not reported again by a later call
     return fail(CNTGW_ECUDA, "softmin launch: %s", cudaGetErrorString(e));

@@ -1,0 +1,295 @@
+// K1/K2 on the 5th-generation tensor cores: the half-update for well-scaled
+// problems with K >= 8 dot features (the C2 micro-benchmark shape).
+//
+// t_ij = beta_j + sum_k x_ik (2 lam z_jk) is a GEMM-shaped score, evaluated as
+// a split-precision ("3xTF32") tcgen05 MMA so that it keeps ~fp32 accuracy:
+//     A'_i = [hi(x_i), 1 | hi(x_i), 1 | lo(x_i), 0]      (K' = 3 KD + 2, padded to 8)
+//     B'_j = [hi(zt_j), hi(b_j) | lo(zt_j), lo(b_j) | hi(zt_j), 0]
+//     A'_i . B'_j = hi.hi + hi.lo + lo.hi  (+ the bias, split exactly)
+// with hi = tf32 rounding and lo = tf32(x - hi). The accumulator lives in
+// TMEM (128 lanes = rows x 256 fp32 columns, double-buffered = all 512 TMEM
+// columns), so the FMA pipe does only the online log-sum-exp epilogue:
+// tcgen05.ld -> subtract the lazily rebased row reference -> MUFU.EX2 -> sum.
+//
+// Warp roles (one CTA per SM, 128 rows x one column chunk):
+//   warp 0      TMA producer: 1-D bulk copies of prepacked B' tiles (56 KB for
+//               KD=16) into a 2-stage shared-memory ring (mbarrier full/empty)
+//   warp 1      TMEM allocator + MMA issuer: one elected lane issues
+//               tcgen05.mma.kind::tf32 (M=128, N=256, K=8 per instruction) and
+//               tcgen05.commit to release the smem stage and publish the tile
+//   warps 2..9  epilogue: warp w reads TMEM lane quadrant w%4 (32 rows) and
+//               column half (w-2)/4 of each tile (32x32b.x32 loads)
+// Operands use the canonical K-major no-swizzle layout: 8-row x 16-byte core
+// matrices, SBO = 128 B between 8-row groups, LBO = rows*16 B between the two
+// 16-byte K chunks of one K=8 MMA step.
+#pragma once
+
+#include "common.cuh"
+#include "softmin.cuh"
+
+namespace cntgw {
+
+constexpr int kTcRows = 128;   // rows per CTA (= TMEM lanes)
+constexpr int kTcCols = 256;   // columns per tile (= MMA N)
+constexpr int kTcThreads = 320;
+
+template <int KD>
+struct TcLayout {
+  static constexpr int kKp = (3 * KD + 2 + 7) / 8 * 8;  // K' padded to the MMA K step
+  static constexpr int kChunks = kKp / 4;                // 16-byte K chunks
+  static constexpr int kBTileFloats = kChunks * kTcCols * 4;
+  static constexpr int kATileFloats = kChunks * kTcRows * 4;
+  // K' positions of the three blocks
+  static constexpr int kHi = 0, kLo = KD + 1, kHi2 = 2 * KD + 2;
+};
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// -- tcgen05 wrappers ----------------------------------------------------------
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  // base_offset 0, lbo_mode 0, layout_type 0 = SWIZZLE_NONE (K-major interleave)
+  return d;
+}
+
+// kind::tf32, fp32 accumulate, A/B K-major, M=128, N=256
+constexpr uint32_t kTcIdesc = (1u << 4)            // c_format F32
+                              | (2u << 7)          // a_format TF32
+                              | (2u << 10)         // b_format TF32
+                              | ((uint32_t)(kTcCols >> 3) << 17)
+                              | ((uint32_t)(kTcRows >> 4) << 24);
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kTcIdesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t* u = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]),
+        "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]),
+        "=r"(u[14]), "=r"(u[15]), "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]),
+        "=r"(u[20]), "=r"(u[21]), "=r"(u[22]), "=r"(u[23]), "=r"(u[24]), "=r"(u[25]),
+        "=r"(u[26]), "=r"(u[27]), "=r"(u[28]), "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Pack the column side in the B' tile layout [tile][chunk][256 cols][4 floats].
+template <int KD>
+__global__ void prep_cols_tc_kernel(const cntgw_sweep_state* st, const float* feat, int64_t ld,
+                                    const double* pot, const double* log2w, int64_t m,
+                                    int64_t mpad, float* rec) {
+  using L = TcLayout<KD>;
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= mpad) return;
+  const int64_t tile = j / kTcCols;
+  const int col = (int)(j % kTcCols);
+  float* base = rec + tile * L::kBTileFloats + col * 4;
+  auto put = [&](int p, float v) { base[(p >> 2) * (kTcCols * 4) + (p & 3)] = v; };
+  for (int p = 0; p < L::kKp; ++p) put(p, 0.f);
+  if (j < m) {
+    const double lam = (double)st->lam;
+    const float two_lam = (float)(2.0 * lam);
+    for (int k = 0; k < KD; ++k) {
+      const float z = two_lam * feat[j * ld + k];
+      const float zh = tf32_rna(z);
+      const float zl = tf32_rna(z - zh);
+      put(L::kHi + k, zh);
+      put(L::kLo + k, zl);
+      put(L::kHi2 + k, zh);
+    }
+    const float beta = (float)(lam * (pot ? pot[j] : 0.0) + log2w[j]);
+    const float bh = tf32_rna(beta);
+    put(L::kHi + KD, bh);
+    put(L::kLo + KD, tf32_rna(beta - bh));
+  } else {
+    put(L::kHi + KD, -1.0e30f);  // padding column: 2^(t - max) == 0
+  }
+}
+
+template <int KD>
+__global__ void __launch_bounds__(kTcThreads, 1) softmin_tc_kernel(const SoftminArgs a) {
+  using L = TcLayout<KD>;
+  extern __shared__ __align__(1024) float smem_tc[];
+  __shared__ uint64_t full_bar[2], empty_bar[2], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ float red_m[kTcRows];
+  __shared__ double red_s[kTcRows];
+  if (skip_now(a.st, a.skip)) return;
+
+  float* sA = smem_tc;                       // A' : kChunks x 128 rows x 16 B
+  float* sB = smem_tc + L::kATileFloats;     // B' : 2 stages
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int chunk = blockIdx.y;
+  const int64_t row0 = (int64_t)blockIdx.x * kTcRows;
+  const int64_t c0 = (int64_t)chunk * a.chunk_cols;
+  const int64_t mpad = (a.m + kColTile - 1) / kColTile * kColTile;
+  const int ntiles = (int)((min(c0 + a.chunk_cols, mpad) - c0) / kTcCols);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {  // TMEM: two 128 x 256 fp32 accumulators
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(&tmem_base_sh)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // A' rows (epilogue warps): hi/lo split of this CTA's row features
+  if (warp >= 2) {
+    const int t = threadIdx.x - 64;
+    const int r = t & (kTcRows - 1), h = t >> 7;
+    const int64_t i = row0 + r;
+    const float* xf = static_cast<const float*>(a.row_feat);
+    auto put = [&](int p, float v) { sA[(p >> 2) * (kTcRows * 4) + r * 4 + (p & 3)] = v; };
+    for (int k = h * (KD / 2); k < (h + 1) * (KD / 2); ++k) {
+      const float x = i < a.n ? xf[i * a.ld_row + k] : 0.f;
+      const float xh = tf32_rna(x);
+      put(L::kHi + k, xh);
+      put(L::kLo + k, xh);
+      put(L::kHi2 + k, tf32_rna(x - xh));
+    }
+    if (h == 0) {
+      put(L::kHi + KD, 1.f);
+      put(L::kLo + KD, 1.f);
+      for (int p = L::kHi2 + KD; p < L::kKp; ++p) put(p, 0.f);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> tensor-core proxy
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      const uint32_t bytes = L::kBTileFloats * sizeof(float);
+      const float* src = static_cast<const float*>(a.col_rec) + (c0 / kTcCols) * L::kBTileFloats;
+      for (int t = 0; t < ntiles; ++t) {
+        const int s = t & 1;
+        mbar_wait(&empty_bar[s], ((t >> 1) & 1) ^ 1);
+        mbar_expect_tx(&full_bar[s], bytes);
+        bulk_g2s(sB + s * L::kBTileFloats, src + (int64_t)t * L::kBTileFloats, bytes, &full_bar[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      const uint32_t a0 = smem_u32(sA);
+      for (int t = 0; t < ntiles; ++t) {
+        const int s = t & 1;
+        mbar_wait(&full_bar[s], (t >> 1) & 1);
+        mbar_wait(&tempty_bar[s], ((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t b0 = smem_u32(sB + s * L::kBTileFloats);
+        const uint32_t d = tmem + (uint32_t)(s * kTcCols);
+#pragma unroll
+        for (int ks = 0; ks < L::kKp / 8; ++ks) {
+          const uint64_t ad = umma_desc(a0 + ks * 2 * (kTcRows * 16), kTcRows * 16, 128);
+          const uint64_t bd = umma_desc(b0 + ks * 2 * (kTcCols * 16), kTcCols * 16, 128);
+          tc_mma(d, ad, bd, ks > 0 ? 1u : 0u);
+        }
+        tc_commit(&empty_bar[s]);  // smem stage reusable once these MMAs completed
+        tc_commit(&tfull_bar[s]);  // accumulator s ready for the epilogue
+      }
+    }
+  } else {  // epilogue warps 2..9
+    const int q = warp & 3;             // TMEM lane quadrant (rows 32q..32q+31)
+    const int half = (warp - 2) >> 2;   // column half of each tile
+    float mref = -CUDART_INF_F;
+    double S = 0.0;
+    for (int t = 0; t < ntiles; ++t) {
+      const int s = t & 1;
+      mbar_wait(&tfull_bar[s], (t >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(s * kTcCols + half * 128);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float v[32];
+        tmem_ld32(taddr + c * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int g = 0; g < 32; g += 8) {
+          float gs = 0.f;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) gs += ex2(v[g + u] - mref);
+          if (!(gs <= kRebase)) {
+            float gm = v[g];
+#pragma unroll
+            for (int u = 1; u < 8; ++u) gm = fmaxf(gm, v[g + u]);
+            if (gm > mref) {
+              S *= (double)ex2(mref - gm);
+              mref = gm;
+            }
+            gs = 0.f;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) gs += ex2(v[g + u] - mref);
+          }
+          S += (double)gs;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[s]);
+    }
+    // merge the two column halves of each row, then store
+    const int r = 32 * q + lane;
+    if (half == 1) {
+      red_m[r] = mref;
+      red_s[r] = S;
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps only
+    if (half == 0) {
+      const float m2 = red_m[r];
+      const double s2 = red_s[r];
+      const float mm = fmaxf(mref, m2);
+      double tot = 0.0;
+      if (S > 0.0) tot += S * exp2((double)(mref - mm));
+      if (s2 > 0.0) tot += s2 * exp2((double)(m2 - mm));
+      const int64_t i = row0 + r;
+      if (i < a.n) softmin_store(a, chunk, i, (double)mm, tot, 1.0 / (double)a.st->lam);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+}  // namespace cntgw

@@ -29,7 +29,7 @@ import numpy as np
 import torch
 
 from . import _native
-from ._native import F32, F64, LIB, SweepStateStruct, call
+from ._native import F32, F64, LIB, TF32X3, SweepStateStruct, call
 
 SUPPORTED_KD = (1, 2, 3, 4, 8, 16, 32, 64)
 # fp32 exponent assembly is used while lam * (term magnitudes) stays below this
@@ -99,13 +99,23 @@ def exponent_scale(eps: float, feat_r, sq_r, feat_c, sq_c, pot_abs: float = 0.0)
     return lam * (pot_abs + dot + sq)
 
 
-def choose_precision(scale: float) -> int:
+def tc_supported(kd: int, sq: bool) -> bool:
+    """Shapes the tcgen05 3xTF32 half-update serves (include/cntgw_b200.h)."""
+    return kd in (8, 16) and not sq
+
+
+def choose_precision(scale: float, kd: int = 0, sq: bool = True) -> int:
+    """fp64 for cold problems; otherwise the tensor cores where the shape allows."""
     forced = os.environ.get("CNTGW_PRECISION", "auto").lower()
     if forced in ("f32", "fp32"):
         return F32
     if forced in ("f64", "fp64"):
         return F64
-    return F32 if scale < F32_EXPONENT_LIMIT else F64
+    if forced in ("tc", "tf32x3"):
+        return TF32X3 if tc_supported(kd, sq) else F32
+    if scale >= F32_EXPONENT_LIMIT:
+        return F64
+    return TF32X3 if tc_supported(kd, sq) else F32
 
 
 class SweepState:
@@ -168,6 +178,7 @@ class Side:
                 self._f32[1].copy_(self.sq64)
 
     def feat(self, prec):
+        """(features, sq) in the dtype the precision path reads (TF32X3 reads fp32)."""
         if prec == F64:
             return self.feat64, self.sq64
         if self._f32 is None:
@@ -184,10 +195,15 @@ class HalfUpdate:
         assert cols.kd == self.kd
         self.prec = prec
         dev = rows.feat64.device
-        stride64 = LIB.cntgw_col_stride(F64, self.kd, int(self.sq))
-        _native.check(0 if stride64 > 0 else stride64, "cntgw_col_stride")
-        self.rec = torch.empty(LIB.cntgw_cols_padded(cols.n) * stride64, dtype=torch.float64, device=dev)
-        wsb = max(LIB.cntgw_softmin_workspace(p, rows.n, cols.n, self.kd, int(self.sq)) for p in (F32, F64))
+        precs = (F32, F64, TF32X3) if tc_supported(self.kd, self.sq) else (F32, F64)
+        rec_bytes = 0
+        for p in precs:
+            stride = LIB.cntgw_col_stride(p, self.kd, int(self.sq))
+            _native.check(0 if stride > 0 else stride, "cntgw_col_stride")
+            rec_bytes = max(rec_bytes, stride * (8 if p == F64 else 4))
+        self.rec = torch.empty(LIB.cntgw_cols_padded(cols.n) * rec_bytes // 8, dtype=torch.float64,
+                               device=dev)
+        wsb = max(LIB.cntgw_softmin_workspace(p, rows.n, cols.n, self.kd, int(self.sq)) for p in precs)
         self.ws = torch.empty(max(int(wsb), 16), dtype=torch.uint8, device=dev)
 
     def pack(self, state: SweepState, pot_cols: torch.Tensor | None, prec=None):

@@ -230,7 +230,7 @@ class _GwDevice:
     def choose_precision(self, f, g, eps_min):
         pot = float(torch.maximum(f.abs().max(), g.abs().max()))
         scale = engine.exponent_scale(eps_min, self.src.feat64, self.sx, self.tgt.feat64, self.ty, pot)
-        self.prec = engine.choose_precision(scale)
+        self.prec = engine.choose_precision(scale, self.kd, True)
         self.loop.set_precision(self.prec)
 
     # -- one outer step ------------------------------------------------------

@@ -142,3 +142,20 @@ def test_c2_full_size_g_update_given_gpu_f(env, c2_full):
     cost_t = O.LowRank(inst.v, inst.u, inst.col_sep, inst.row_sep)
     want = O.softmin(cost_t, np.full(n, -np.log(n)), res.coupling.f, inst.eps, row_idx=cols)
     assert _rel(res.coupling.g[cols], want) < 1e-5
+
+
+@pytest.mark.parametrize("prec", [0, 2], ids=["f32", "tc"])
+@pytest.mark.parametrize("k", [8, 16])
+@pytest.mark.parametrize("n,m", [(1, 1), (129, 257), (1000, 1000), (2049, 771), (300, 5000)])
+def test_low_rank_paths(env, prec, k, n, m):
+    """fp32 FFMA2 and tcgen05 3xTF32 half-updates on the C2 cost form."""
+    P, engine, S, O, torch, dev = env
+    from paper_2602_06658_b200 import configs
+
+    inst = configs.c2(seed=n + m + k, n=n, m=m, k=k)
+    a, b = np.full(n, 1 / n), np.full(m, 1 / m)
+    cost = P.SeparableLowRankCost(inst.u, inst.v, inst.row_sep, inst.col_sep)
+    got = _half_update(env, cost, a, b, inst.g.astype(float) + inst.col_sep, inst.eps, prec)
+    want = O.softmin(O.LowRank(inst.u, inst.v, inst.row_sep, inst.col_sep), np.log(b),
+                     inst.g.astype(float) + inst.col_sep, inst.eps)
+    assert _rel(got, want) < 1e-5
