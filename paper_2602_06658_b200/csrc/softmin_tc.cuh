@@ -137,6 +137,41 @@ __global__ void prep_cols_tc_kernel(const cntgw_sweep_state* st, const float* fe
   }
 }
 
+// One 32-column chunk of the epilogue: terms 2^(v - mref) summed with FADD2
+// pairs into four independent accumulators; a chunk whose sum leaves [0, 2^20]
+// (or is inf/NaN) rebases the row reference at the chunk maximum.
+__device__ __forceinline__ void tc_chunk(const float (&v)[32], float& mref, float& tsum, double& S) {
+  float2 nm = f2(-mref, -mref);
+  float2 acc[4] = {f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f)};
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const float2 x = add2(f2(v[2 * u], v[2 * u + 1]), nm);
+    acc[u & 3] = add2(acc[u & 3], f2(ex2(x.x), ex2(x.y)));
+  }
+  float2 t2 = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+  float csum = t2.x + t2.y;
+  if (!(csum <= 1048576.0f)) {
+    float cm = v[0];
+#pragma unroll
+    for (int u = 1; u < 32; ++u) cm = fmaxf(cm, v[u]);
+    if (cm > mref) {
+      const float sc = ex2(mref - cm);
+      S *= (double)sc;
+      tsum *= sc;
+      mref = cm;
+    }
+    nm = f2(-mref, -mref);
+    float2 r = f2(0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const float2 x = add2(f2(v[2 * u], v[2 * u + 1]), nm);
+      r = add2(r, f2(ex2(x.x), ex2(x.y)));
+    }
+    csum = r.x + r.y;
+  }
+  tsum += csum;
+}
+
 template <int KD>
 __global__ void __launch_bounds__(kTcThreads, 1) softmin_tc_kernel(const SoftminArgs a) {
   using L = TcLayout<KD>;
@@ -230,41 +265,32 @@ __global__ void __launch_bounds__(kTcThreads, 1) softmin_tc_kernel(const Softmin
   } else {  // epilogue warps 2..9
     const int q = warp & 3;             // TMEM lane quadrant (rows 32q..32q+31)
     const int half = (warp - 2) >> 2;   // column half of each tile
-    float mref = -CUDART_INF_F;
-    double S = 0.0;
+    float mref = -CUDART_INF_F;         // lazily rebased row reference (log2 units)
+    double S = 0.0;                     // sum over finished tiles of 2^(t - mref)
+    float va[32], vb[32];
     for (int t = 0; t < ntiles; ++t) {
       const int s = t & 1;
       mbar_wait(&tfull_bar[s], (t >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(s * kTcCols + half * 128);
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        float v[32];
-        tmem_ld32(taddr + c * 32, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int g = 0; g < 32; g += 8) {
-          float gs = 0.f;
-#pragma unroll
-          for (int u = 0; u < 8; ++u) gs += ex2(v[g + u] - mref);
-          if (!(gs <= kRebase)) {
-            float gm = v[g];
-#pragma unroll
-            for (int u = 1; u < 8; ++u) gm = fmaxf(gm, v[g + u]);
-            if (gm > mref) {
-              S *= (double)ex2(mref - gm);
-              mref = gm;
-            }
-            gs = 0.f;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) gs += ex2(v[g + u] - mref);
-          }
-          S += (double)gs;
-        }
-      }
+      float tsum = 0.f;  // this tile's sum against mref (fp32; folded into S per tile)
+      tmem_ld32(taddr, va);
+      tmem_wait_ld();
+      // four 32-column chunks; the next chunk's TMEM load overlaps this chunk's math
+      tmem_ld32(taddr + 32, vb);
+      tc_chunk(va, mref, tsum, S);
+      tmem_wait_ld();
+      tmem_ld32(taddr + 64, va);
+      tc_chunk(vb, mref, tsum, S);
+      tmem_wait_ld();
+      tmem_ld32(taddr + 96, vb);
+      tc_chunk(va, mref, tsum, S);
+      tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[s]);
+      if (lane == 0) mbar_arrive(&tempty_bar[s]);  // accumulator s may be overwritten
+      tc_chunk(vb, mref, tsum, S);
+      S += (double)tsum;
     }
     // merge the two column halves of each row, then store
     const int r = 32 * q + lane;
