@@ -115,9 +115,12 @@ int cntgw_sweep_apply(const cntgw_sweep_state* st, double* pot, const double* te
 
 /* ---- K1/K2: half-update (sinkhorn.py:166-176) ---------------------------- */
 /* Pack the column side for the current lam of `st`, sign-flipped so the
- * kernels accumulate with plain FMAs: [-2 lam z (kd) | -sqrt(lam) s (if sq) |
- * -(lam pot + log2 w) | zero pad]. Padding columns m..cols_padded(m)-1 get an
- * exactly-zero weight. feat: m x kd row-major (stride ld), fp32 or fp64 per
+ * kernels accumulate with plain FMAs: fp32 [-2 lam z (kd) | -sqrt(lam) s (if
+ * sq) | -(lam pot + log2 w) | zero pad] (squared coordinate kept as a
+ * difference); fp64 [-2 lam z | -2 lam s | -(lam (pot - s^2) + log2 w)]
+ * (square expanded, exact enough in fp64); tensor-core: 3xTF32 tiles (see
+ * softmin_tc.cuh). Padding columns m..cols_padded(m)-1 get an exactly-zero
+ * weight. feat: m x kd row-major (stride ld), fp32 or fp64 per
  * prec, as is sq; pot (nullable => 0) and log2w are fp64. */
 int cntgw_prep_cols(const cntgw_sweep_state* st, int prec, int kd, int sq_flag, const void* feat,
                     int64_t ld, const void* sq, const double* pot, const double* log2w, int64_t m,

@@ -2,6 +2,7 @@
 // half-update dispatch (fp32 / fp64 paths), workspace sizing and error
 // reporting. Declarations and contracts: include/cntgw_b200.h.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 
@@ -105,14 +106,35 @@ KernelPick pick() {
   X(PREC, 4, 0) X(PREC, 4, 1) X(PREC, 8, 0) X(PREC, 8, 1) X(PREC, 16, 0) X(PREC, 16, 1) \
   X(PREC, 32, 0) X(PREC, 32, 1) X(PREC, 64, 0) X(PREC, 64, 1)
 
+// Tensor-core variant knobs (read per call so tools can sweep them):
+// CNTGW_TC_POLY in {0,2,4,6} (default 2, fastest in tools/sweep_paths.py):
+// pairs (of 16 per 32-column chunk) whose exp2 runs on the FMA pipe instead of
+// MUFU; CNTGW_TC_EPI in {8,16}: epilogue warps (default 8).
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+template <int KD, int EPI>
+void* tc_fn(int poly) {
+  switch (poly) {
+    case 2: return (void*)softmin_tc_kernel<KD, 2, EPI>;
+    case 4: return (void*)softmin_tc_kernel<KD, 4, EPI>;
+    case 6: return (void*)softmin_tc_kernel<KD, 6, EPI>;
+    default: return (void*)softmin_tc_kernel<KD, 0, EPI>;
+  }
+}
+
 template <int KD>
 KernelPick pick_tc() {
   using L = TcLayout<KD>;
   KernelPick k;
-  k.fn = (void*)softmin_tc_kernel<KD>;
+  const int poly = env_int("CNTGW_TC_POLY", 2);
+  const int epi = env_int("CNTGW_TC_EPI", 8) == 16 ? 16 : 8;
+  k.fn = epi == 16 ? tc_fn<KD, 16>(poly) : tc_fn<KD, 8>(poly);
   k.rows = 1;  // 128 rows per CTA = 128 threads x 1 in the planner's units
   k.smem = (size_t)(L::kATileFloats + 2 * L::kBTileFloats) * sizeof(float);
-  k.threads = kTcThreads;
+  k.threads = tc_threads(epi);
   return k;
 }
 
@@ -190,8 +212,16 @@ __global__ void prep_cols_kernel(const cntgw_sweep_state* st, int kd, int sq_fla
   if (j < m) {
     const T two_lam = (T)(2.0 * lam);
     for (int k = 0; k < kd; ++k) r[k] = -two_lam * feat[j * ld + k];
-    if (sq_flag) r[kd] = (T)(-sl) * sq[j];
-    const double beta = lam * (pot ? pot[j] : 0.0) + log2w[j];
+    double beta = lam * (pot ? pot[j] : 0.0) + log2w[j];
+    if (sq_flag) {
+      if (f64) {  // expanded square: -2 lam s_j multiplies the raw row s_i
+        const double sj = (double)sq[j];
+        r[kd] = (T)(-2.0 * lam * sj);
+        beta -= lam * sj * sj;
+      } else {  // difference form: sqrt(lam) s_j, squared against sqrt(lam) s_i
+        r[kd] = (T)(-sl) * sq[j];
+      }
+    }
     r[kd + sq_flag] = (T)(-beta);
   } else {
     for (int k = 0; k < kd + sq_flag; ++k) r[k] = (T)0;
@@ -345,12 +375,7 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
   KernelPick k;
   if (!lookup(prec, kd, sq_flag, &k))
     return fail(CNTGW_EINVAL, "softmin: unsupported precision %d / feature width kd=%d", prec, kd);
-  static bool attr_done[3][65][2] = {};
-  bool& done = attr_done[prec % 3][kd][sq_flag ? 1 : 0];
-  if (!done) {
-    cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem);
-    done = true;
-  }
+  cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem);
   const Plan p = plan_softmin(n, m, k);
   SoftminArgs a{};
   a.st = st;

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(128) plan_reduce_kernel(const PlanReduceArgs a
   double x[KD];
 #pragma unroll
   for (int k = 0; k < KD; ++k) x[k] = live ? a.row_feat[i * a.ld_row + k] : 0.0;
-  const double s = live ? a.st->sqrt_lam_d * a.row_sq[i] : 0.0;
+  const double s = live ? a.row_sq[i] : 0.0;
 
   double mq = kStartQ, S = 0.0, acc_s = 0.0, qbest = CUDART_INF;
   double acc_y[E];
@@ -90,8 +90,7 @@ __global__ void __launch_bounds__(128) plan_reduce_kernel(const PlanReduceArgs a
         double acc = c[L::kBeta];
 #pragma unroll
         for (int k = 0; k < KD; ++k) acc = fma(x[k], c[k], acc);
-        const double u = s + c[KD];
-        acc = fma(u, u, acc);
+        acc = fma(s, c[KD], acc);  // expanded square; lam s_i^2 is a row constant
         q[g] = acc;
         if (acc < qbest) {  // strict: the first (lowest) j wins ties, numpy.argmax rule
           qbest = acc;
@@ -134,7 +133,7 @@ __global__ void __launch_bounds__(128) plan_reduce_kernel(const PlanReduceArgs a
   }
   if (!live) return;
   // pi_ij = a_i 2^(lam f~_i) 2^(t_ij) and sum_j 2^(t_ij) = 2^(-mq) S
-  const double scale = exp2(a.st->lam_d * a.f_tilde[i] + a.log2a[i] - mq);
+  const double scale = exp2(a.st->lam_d * (a.f_tilde[i] - s * s) + a.log2a[i] - mq);
   a.row_mass[i] = S * scale;
   a.pi_s[i] = acc_s * scale;
 #pragma unroll

@@ -19,8 +19,10 @@
 //
 //  * fp32 path: rows packed in pairs, q assembled with FFMA2/FADD2
 //    (KD/2 + 1.5 FP32 instructions per pair).
-//  * fp64 path: q assembled with DFMA (KD + 3 fp64 ops per pair; B200 runs
-//    fp64 at half the fp32 rate), the small difference mq - q converted to
+//  * fp64 path: q assembled with DFMA (KD + 2 fp64 ops per pair: in fp64 the
+//    squared coordinate is expanded, (s_i - s_j)^2 -> -2 s_i s_j + s_j^2 with the
+//    s_i^2 row constant re-added at the end; B200 runs fp64 at half the fp32
+//    rate), the small difference mq - q converted to
 //    fp32 on the integer ALU (f64_to_f32_alu) and exponentiated on MUFU. This
 //    is the path for cold problems where |t_ij| ~ 1e6-1e7 log2 units (C4/C5):
 //    fp32 rounding there is 0.06-1 log2 units per plan entry.
@@ -235,10 +237,7 @@ __device__ __forceinline__ void softmin_tile_f64(const double* __restrict__ rec,
         double acc = c[L::kBeta];
 #pragma unroll
         for (int k = 0; k < KD; ++k) acc = fma(x[r][k], c[k], acc);
-        if (SQ) {
-          const double u = s[r] + c[KD];
-          acc = fma(u, u, acc);
-        }
+        if (SQ) acc = fma(s[r], c[KD], acc);  // -2 lam s_i t_j; lam s_i^2 added per row
         q[r][g] = acc;
       }
     }
@@ -274,7 +273,6 @@ __global__ void __launch_bounds__(128, MINB) softmin_f64_kernel(const SoftminArg
 
   const int chunk = blockIdx.y;
   const int64_t row0 = (int64_t)blockIdx.x * (128 * R) + threadIdx.x;
-  const double sl = a.st->sqrt_lam_d;
   const double* rf = static_cast<const double*>(a.row_feat);
   const double* rs = static_cast<const double*>(a.row_sq);
   double x[R][KD], s[R], mq[R], S[R];
@@ -284,7 +282,7 @@ __global__ void __launch_bounds__(128, MINB) softmin_f64_kernel(const SoftminArg
     const bool ok = i < a.n;
 #pragma unroll
     for (int k = 0; k < KD; ++k) x[r][k] = ok ? rf[i * a.ld_row + k] : 0.0;
-    s[r] = (SQ && ok) ? sl * rs[i] : 0.0;
+    s[r] = (SQ && ok) ? rs[i] : 0.0;
     mq[r] = kStartQ;
     S[r] = 0.0;
   }
@@ -311,11 +309,12 @@ __global__ void __launch_bounds__(128, MINB) softmin_f64_kernel(const SoftminArg
       bulk_g2s(smem_d + sb * kStage, src + (int64_t)(t + 2) * kStage, bytes, &bars[sb]);
     }
   }
-  const double inv_lam = 1.0 / a.st->lam_d;
+  const double lam = a.st->lam_d, inv_lam = 1.0 / lam;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t i = row0 + (int64_t)r * 128;
-    if (i < a.n) softmin_store(a, chunk, i, -mq[r], S[r], inv_lam);
+    // q accumulated without the row constant lam s_i^2 (expanded square)
+    if (i < a.n) softmin_store(a, chunk, i, -mq[r] - (SQ ? lam * s[r] * s[r] : 0.0), S[r], inv_lam);
   }
 }
 

@@ -17,8 +17,9 @@
 //   warp 1      TMEM allocator + MMA issuer: one elected lane issues
 //               tcgen05.mma.kind::tf32 (M=128, N=256, K=8 per instruction) and
 //               tcgen05.commit to release the smem stage and publish the tile
-//   warps 2..9  epilogue: warp w reads TMEM lane quadrant w%4 (32 rows) and
-//               column half (w-2)/4 of each tile (32x32b.x32 loads)
+//   warps 2..   EPI epilogue warps: warp w reads TMEM lane quadrant w%4 (32
+//               rows) and column part (w-2)/4 of each tile (32x32b.x32 loads,
+//               the next chunk's load in flight while the current is consumed)
 // Operands use the canonical K-major no-swizzle layout: 8-row x 16-byte core
 // matrices, SBO = 128 B between 8-row groups, LBO = rows*16 B between the two
 // 16-byte K chunks of one K=8 MMA step.
@@ -31,7 +32,8 @@ namespace cntgw {
 
 constexpr int kTcRows = 128;   // rows per CTA (= TMEM lanes)
 constexpr int kTcCols = 256;   // columns per tile (= MMA N)
-constexpr int kTcThreads = 320;
+// producer + MMA warps + EPI epilogue warps (EPI/4 per TMEM lane quadrant)
+constexpr int tc_threads(int epi) { return 64 + 32 * epi; }
 
 template <int KD>
 struct TcLayout {
@@ -137,16 +139,44 @@ __global__ void prep_cols_tc_kernel(const cntgw_sweep_state* st, const float* fe
   }
 }
 
+// 2^x for two values on the FMA pipe (FA4-style MUFU offload): x clamped to
+// [-125, 64], split x = j + r with |r| <= 1/2 by the 1.5*2^23 rounding trick,
+// 2^r by a degree-5 minimax polynomial (max rel. error 2.3e-7 in fp32 Horner,
+// on par with MUFU.EX2), and j added to the exponent field with an integer op.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fminf(fmaxf(x.x, -125.f), 64.f);
+  x.y = fminf(fmaxf(x.y, -125.f), 64.f);
+  const float2 t = add2(x, f2(12582912.f, 12582912.f));
+  const float2 j = add2(t, f2(-12582912.f, -12582912.f));
+  const float2 r = fma2(j, f2(-1.f, -1.f), x);
+  float2 p = f2(1.3276470126584172e-3f, 1.3276470126584172e-3f);
+  p = fma2(p, r, f2(9.675541892647743e-3f, 9.675541892647743e-3f));
+  p = fma2(p, r, f2(5.550713464617729e-2f, 5.550713464617729e-2f));
+  p = fma2(p, r, f2(0.24022120237350464f, 0.24022120237350464f));
+  p = fma2(p, r, f2(0.6931469440460205f, 0.6931469440460205f));
+  p = fma2(p, r, f2(1.0000001192092896f, 1.0000001192092896f));
+  return f2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+            __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+
 // One 32-column chunk of the epilogue: terms 2^(v - mref) summed with FADD2
-// pairs into four independent accumulators; a chunk whose sum leaves [0, 2^20]
+// pairs into four independent accumulators, NPOLY of the 16 pairs exponentiated
+// on the FMA pipe and the rest on MUFU.EX2; a chunk whose sum leaves [0, 2^20]
 // (or is inf/NaN) rebases the row reference at the chunk maximum.
+template <int NPOLY>
 __device__ __forceinline__ void tc_chunk(const float (&v)[32], float& mref, float& tsum, double& S) {
   float2 nm = f2(-mref, -mref);
   float2 acc[4] = {f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f)};
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
     const float2 x = add2(f2(v[2 * u], v[2 * u + 1]), nm);
-    acc[u & 3] = add2(acc[u & 3], f2(ex2(x.x), ex2(x.y)));
+    // offloaded pairs spread over the four accumulators
+    constexpr uint32_t kMask = NPOLY == 2   ? 0x0201u
+                               : NPOLY == 4 ? 0x8421u
+                               : NPOLY == 6 ? 0x9249u
+                                            : 0u;
+    const bool poly = (kMask >> u) & 1u;
+    acc[u & 3] = add2(acc[u & 3], poly ? exp2_poly2(x) : f2(ex2(x.x), ex2(x.y)));
   }
   float2 t2 = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
   float csum = t2.x + t2.y;
@@ -172,14 +202,16 @@ __device__ __forceinline__ void tc_chunk(const float (&v)[32], float& mref, floa
   tsum += csum;
 }
 
-template <int KD>
-__global__ void __launch_bounds__(kTcThreads, 1) softmin_tc_kernel(const SoftminArgs a) {
+template <int KD, int NPOLY, int EPI>
+__global__ void __launch_bounds__(tc_threads(EPI), 1) softmin_tc_kernel(const SoftminArgs a) {
   using L = TcLayout<KD>;
   extern __shared__ __align__(1024) float smem_tc[];
   __shared__ uint64_t full_bar[2], empty_bar[2], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ float red_m[kTcRows];
-  __shared__ double red_s[kTcRows];
+  constexpr int kParts = EPI / 4;                  // column parts per TMEM quadrant
+  constexpr int kChunksPerPart = kTcCols / kParts / 32;
+  __shared__ float red_m[kParts][kTcRows];
+  __shared__ double red_s[kParts][kTcRows];
   if (skip_now(a.st, a.skip)) return;
 
   float* sA = smem_tc;                       // A' : kChunks x 128 rows x 16 B
@@ -196,7 +228,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) softmin_tc_kernel(const Softmin
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 8);
+      mbar_init(&tempty_bar[s], EPI);
     }
     fence_mbar_init();
   }
@@ -212,7 +244,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) softmin_tc_kernel(const Softmin
     const int64_t i = row0 + r;
     const float* xf = static_cast<const float*>(a.row_feat);
     auto put = [&](int p, float v) { sA[(p >> 2) * (kTcRows * 4) + r * 4 + (p & 3)] = v; };
-    for (int k = h * (KD / 2); k < (h + 1) * (KD / 2); ++k) {
+    for (int k = h * (KD / kParts); k < (h + 1) * (KD / kParts); ++k) {
       const float x = i < a.n ? xf[i * a.ld_row + k] : 0.f;
       const float xh = tf32_rna(x);
       put(L::kHi + k, xh);
@@ -262,9 +294,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) softmin_tc_kernel(const Softmin
         tc_commit(&tfull_bar[s]);  // accumulator s ready for the epilogue
       }
     }
-  } else {  // epilogue warps 2..9
+  } else {  // epilogue warps
     const int q = warp & 3;             // TMEM lane quadrant (rows 32q..32q+31)
-    const int half = (warp - 2) >> 2;   // column half of each tile
+    const int part = (warp - 2) >> 2;   // column part of each tile
     float mref = -CUDART_INF_F;         // lazily rebased row reference (log2 units)
     double S = 0.0;                     // sum over finished tiles of 2^(t - mref)
     float va[32], vb[32];
@@ -272,40 +304,40 @@ __global__ void __launch_bounds__(kTcThreads, 1) softmin_tc_kernel(const Softmin
       const int s = t & 1;
       mbar_wait(&tfull_bar[s], (t >> 1) & 1);
       tc_fence_after();
-      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(s * kTcCols + half * 128);
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) +
+                             (uint32_t)(s * kTcCols + part * (kTcCols / kParts));
       float tsum = 0.f;  // this tile's sum against mref (fp32; folded into S per tile)
       tmem_ld32(taddr, va);
       tmem_wait_ld();
-      // four 32-column chunks; the next chunk's TMEM load overlaps this chunk's math
-      tmem_ld32(taddr + 32, vb);
-      tc_chunk(va, mref, tsum, S);
-      tmem_wait_ld();
-      tmem_ld32(taddr + 64, va);
-      tc_chunk(vb, mref, tsum, S);
-      tmem_wait_ld();
-      tmem_ld32(taddr + 96, vb);
-      tc_chunk(va, mref, tsum, S);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[s]);  // accumulator s may be overwritten
-      tc_chunk(vb, mref, tsum, S);
+#pragma unroll
+      for (int c = 0; c < kChunksPerPart; ++c) {
+        float(&cur)[32] = (c & 1) ? vb : va;
+        float(&nxt)[32] = (c & 1) ? va : vb;
+        if (c + 1 < kChunksPerPart) {
+          tmem_ld32(taddr + 32 * (c + 1), nxt);  // overlaps this chunk's math
+        } else {
+          tc_fence_before();  // every TMEM load of this tile has completed
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[s]);  // accumulator s may be overwritten
+        }
+        tc_chunk<NPOLY>(cur, mref, tsum, S);
+        if (c + 1 < kChunksPerPart) tmem_wait_ld();
+      }
       S += (double)tsum;
     }
-    // merge the two column halves of each row, then store
+    // merge the column parts of each row, then store
     const int r = 32 * q + lane;
-    if (half == 1) {
-      red_m[r] = mref;
-      red_s[r] = S;
-    }
-    asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps only
-    if (half == 0) {
-      const float m2 = red_m[r];
-      const double s2 = red_s[r];
-      const float mm = fmaxf(mref, m2);
+    red_m[part][r] = mref;
+    red_s[part][r] = S;
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI) : "memory");  // epilogue warps only
+    if (part == 0) {
+      float mm = red_m[0][r];
+#pragma unroll
+      for (int p = 1; p < kParts; ++p) mm = fmaxf(mm, red_m[p][r]);
       double tot = 0.0;
-      if (S > 0.0) tot += S * exp2((double)(mref - mm));
-      if (s2 > 0.0) tot += s2 * exp2((double)(m2 - mm));
+#pragma unroll
+      for (int p = 0; p < kParts; ++p)
+        if (red_s[p][r] > 0.0) tot += red_s[p][r] * exp2((double)(red_m[p][r] - mm));
       const int64_t i = row0 + r;
       if (i < a.n) softmin_store(a, chunk, i, (double)mm, tot, 1.0 / (double)a.st->lam);
     }
