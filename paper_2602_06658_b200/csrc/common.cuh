@@ -43,6 +43,20 @@ __device__ __forceinline__ float f64_to_f32_alu(double v) {
   return __uint_as_float((f & 0x7fffffffu) | (hi & 0x80000000u));
 }
 
+// Cheaper conversion for the streaming fp64 softmin (3 ALU ops: IADD, SHF,
+// LOP3): the kernel keeps every exponent argument away from zero by carrying
+// its row reference kRefOffset log2 units above the row minimum, so the only
+// "tiny" argument possible is an exact 0, which this maps to +-2.0 instead of
+// 1.0 — an error of < 4 * 2^-kRefOffset relative to the row's largest term.
+constexpr double kRefOffset = 32.0;
+constexpr float kRebaseF64 = 281474976710656.0f;  // 2^(16 + kRefOffset)
+__device__ __forceinline__ float f64_to_f32_fast(double w) {
+  const uint32_t lo = (uint32_t)__double2loint(w);
+  const uint32_t hi = (uint32_t)__double2hiint(w);
+  const uint32_t f = __funnelshift_l(lo, hi - 0x38000000u, 3);
+  return __uint_as_float((f & 0x7fffffffu) | (hi & 0x80000000u));
+}
+
 // Packed fp32x2 arithmetic (sm_100a FFMA2/FADD2): two rows per instruction.
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
   float2 d;

@@ -241,22 +241,25 @@ __device__ __forceinline__ void softmin_tile_f64(const double* __restrict__ rec,
         q[r][g] = acc;
       }
     }
+    // mq is the row reference carried kRefOffset above the smallest q seen, so
+    // terms are 2^(mq - q) in [0, 2^(16 + kRefOffset)] between rebases
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       float gsum = 0.f;
 #pragma unroll
-      for (int g = 0; g < G; ++g) gsum += ex2(f64_to_f32_alu(mq[r] - q[r][g]));
-      if (!(gsum <= kRebase)) {  // rare: rebase at the group minimum
+      for (int g = 0; g < G; ++g) gsum += ex2(f64_to_f32_fast(mq[r] - q[r][g]));
+      if (!(gsum <= kRebaseF64)) {  // rare: rebase at the group minimum
         double qmin = q[r][0];
 #pragma unroll
         for (int g = 1; g < G; ++g) qmin = fmin(qmin, q[r][g]);
-        if (qmin < mq[r]) {
-          S[r] *= exp2(qmin - mq[r]);
-          mq[r] = qmin;
+        const double ref = qmin + kRefOffset;
+        if (ref < mq[r]) {
+          S[r] *= exp2(ref - mq[r]);
+          mq[r] = ref;
         }
         gsum = 0.f;
 #pragma unroll
-        for (int g = 0; g < G; ++g) gsum += ex2(f64_to_f32_alu(mq[r] - q[r][g]));
+        for (int g = 0; g < G; ++g) gsum += ex2(f64_to_f32_fast(mq[r] - q[r][g]));
       }
       S[r] += (double)gsum;
     }

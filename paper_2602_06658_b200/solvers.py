@@ -30,7 +30,9 @@ from dataclasses import dataclass, field, replace
 import numpy as np
 import torch
 
-from . import divergence, engine
+import torch.distributed as tdist
+
+from . import dist, divergence, engine
 from ._native import F32, F64, LIB, call
 from .measures import DenseCoupling, ImplicitCoupling
 from .sinkhorn import SinkhornConfig, SquaredEuclideanCost, sinkhorn
@@ -166,19 +168,30 @@ def _stream():
 
 
 class _GwDevice:
-    """Device buffers and kernels of the feature-space CNT-GW step."""
+    """Device buffers and kernels of the feature-space CNT-GW step.
 
-    def __init__(self, src, tgt, device):
+    With torch.distributed initialised at world size > 1 the source rows are
+    sharded (dist.py): this rank holds rows [lo, hi) of X, f and the plan
+    reductions; Y, g and Gamma are replicated; the g-update and the row
+    reductions go through NCCL all-reduces.
+    """
+
+    def __init__(self, src, tgt, device, info=None):
         self.device = device
+        self.info = info if info is not None else dist.DistInfo()
+        self.comm = dist.RowShardComm(self.info) if self.info.enabled else None
         x = np.asarray(src.features, dtype=np.float64)
         y = np.asarray(tgt.features, dtype=np.float64)
+        self.n_total = x.shape[0]
+        self.lo, self.hi = dist.shard_range(self.n_total, self.info.rank, self.info.world)
+        x = x[self.lo:self.hi]
         self.n, self.d = x.shape
         self.m, self.e = y.shape
         self.x = engine.to_dev64(x, device)
         self.y = engine.to_dev64(y, device)
-        self.sx = engine.to_dev64(_half_sq(src), device)
+        self.sx = engine.to_dev64(_half_sq(src)[self.lo:self.hi], device)
         self.ty = engine.to_dev64(_half_sq(tgt), device)
-        self.a = engine.to_dev64(src.weights, device)
+        self.a = engine.to_dev64(np.asarray(src.weights)[self.lo:self.hi], device)
         self.b = engine.to_dev64(tgt.weights, device)
         self.proj_rows = self.d > self.e  # E-side projection (SURVEY.md §7.3d)
         self.k = min(self.d, self.e)
@@ -193,7 +206,7 @@ class _GwDevice:
         self.tgt = engine.Side(cols_feat, self.ty, self.b)
         self.fwd = engine.HalfUpdate(self.src, self.tgt, True)
         self.bwd = engine.HalfUpdate(self.tgt, self.src, True)
-        self.loop = engine.SinkhornLoop(self.fwd, self.bwd, self.a, self.b, device)
+        self.loop = engine.SinkhornLoop(self.fwd, self.bwd, self.a, self.b, device, comm=self.comm)
         # K4 / K7 buffers
         self.r = torch.empty(self.n, dtype=torch.float64, device=device)
         self.pi_y = torch.empty(self.n * self.e, dtype=torch.float64, device=device)
@@ -227,8 +240,23 @@ class _GwDevice:
     def row_sep(self) -> torch.Tensor:
         return (self.x ** 2).sum(1)
 
+    def gather_rows(self, t: torch.Tensor) -> torch.Tensor:
+        """Full-length copy of a row-sharded vector (all ranks)."""
+        if self.comm is None:
+            return t
+        sizes = [dist.shard_range(self.n_total, r, self.info.world) for r in range(self.info.world)]
+        width = max(h - l for l, h in sizes)
+        buf = torch.zeros(width, dtype=t.dtype, device=t.device)
+        buf[: t.numel()] = t
+        parts = [torch.empty_like(buf) for _ in sizes]
+        tdist.all_gather(parts, buf)
+        return torch.cat([p[: h - l] for p, (l, h) in zip(parts, sizes)])
+
     def choose_precision(self, f, g, eps_min):
-        pot = float(torch.maximum(f.abs().max(), g.abs().max()))
+        fmax = f.abs().max()
+        if self.comm is not None:
+            tdist.all_reduce(fmax, op=tdist.ReduceOp.MAX)
+        pot = float(torch.maximum(fmax, g.abs().max()))
         scale = engine.exponent_scale(eps_min, self.src.feat64, self.sx, self.tgt.feat64, self.ty, pot)
         self.prec = engine.choose_precision(scale, self.kd, True)
         self.loop.set_precision(self.prec)
@@ -258,6 +286,8 @@ class _GwDevice:
         call("cntgw_outer_reduce_cols", st.ptr, g.data_ptr(), self.loop.gt.data_ptr(),
              self.ty.data_ptr(), self.b.data_ptr(), self.m, self.acc[nrow:].data_ptr(),
              self.ws_outer.data_ptr(), self.ws_outer.numel(), stream)
+        if self.comm is not None:  # row-side sums and Gamma_{t+1} over all shards
+            tdist.all_reduce(self.acc[:nrow], op=tdist.ReduceOp.SUM)
         acc = self.acc.cpu().numpy()  # the one host read per outer step
         rows, cols = acc[:16], acc[nrow:]
         gamma_next = acc[16:nrow].reshape(self.d, self.e).copy()
@@ -317,24 +347,30 @@ class _CntGwState:
                 f"beyond the memory guard ({cfg.max_dense_entries})"
             )
         self.device = engine.require_cuda()
-        self.dev = _GwDevice(src, tgt, self.device)
+        info = dist.DistInfo()
+        if tdist.is_available() and tdist.is_initialized() and tdist.get_world_size() > 1:
+            info = dist.DistInfo(rank=tdist.get_rank(), world=tdist.get_world_size(),
+                                 local_rank=self.device.index)
+        self.dev = _GwDevice(src, tgt, self.device, info)
         self.gamma = _initial_gamma(src, tgt, cfg)
         if warm_potentials is None:
             # interaction potentials 0 (solvers.py:297-301): f~ = s^2, g~ = t^2
             self.f = self.dev.sx ** 2
             self.g = self.dev.ty ** 2
         else:
-            f0 = engine.to_dev64(np.asarray(warm_potentials[0], dtype=np.float64), self.device)
+            f0 = np.asarray(warm_potentials[0], dtype=np.float64)[self.dev.lo:self.dev.hi]
+            f0 = engine.to_dev64(f0, self.device)
             g0 = engine.to_dev64(np.asarray(warm_potentials[1], dtype=np.float64), self.device)
             self.f = f0 - self.dev.row_sep()
             self.g = g0 - self.dev.col_sep(self.gamma)
-        mx = divergence.moments(self.dev.x, self.dev.a, self.device).cpu().numpy()
+        mx = divergence.moments(np.asarray(src.features, dtype=np.float64),
+                                np.asarray(src.weights, dtype=np.float64), self.device).cpu().numpy()
         my = divergence.moments(self.dev.y, self.dev.b, self.device).cpu().numpy()
         self.constant = divergence.constant_from_moments(mx, self.dev.d, my, self.dev.e)
         self.coupling_gamma = None
         self.eps_eff = None
         self.record = []
-        self.use_graph = self.dev.n * self.dev.m <= (1 << 24)
+        self.use_graph = self.dev.n * self.dev.m <= (1 << 24) and not info.enabled
 
     def step(self, inner_budget=None, anneal_from=None) -> _StepStats:
         inner = self.cfg.inner
@@ -357,7 +393,7 @@ class _CntGwState:
         """The last plan (built on Gamma_t, solvers.py:326-336) in reference form."""
         dev = self.dev
         gt = self.coupling_gamma
-        f = (self.f + dev.row_sep()).cpu().numpy()
+        f = dev.gather_rows(self.f + dev.row_sep()).cpu().numpy()
         g = (self.g + dev.col_sep(gt)).cpu().numpy()
         src, tgt = self.src, self.tgt
         xbar = np.column_stack([src.features, _half_sq(src)])
@@ -372,7 +408,7 @@ class _CntGwState:
             gamma=self.gamma, coupling=coupling, trace=trace,
             value=trace.objectives[-1] if len(trace) else math.nan, converged=converged,
             iterates=self.record if self.cfg.record_iterates else None, schedule=schedule,
-            argmax=self.dev.argmax.cpu().numpy() if coupling is not None else None,
+            argmax=self.dev.gather_rows(self.dev.argmax).cpu().numpy() if coupling is not None else None,
         )
 
 

@@ -66,7 +66,7 @@ def test_sq_euclidean_half_update(env, k, n, m, prec):
     eps = 0.05
     got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, prec)
     want = O.softmin(O.SqEuclid(x, z), np.log(b), g, eps)
-    assert _rel(got, want) < (1e-5 if prec == 0 else 1e-7)
+    assert _rel(got, want) < (1e-5 if prec == 0 else 5e-7)
 
 
 @pytest.mark.parametrize("k", [4, 16])
@@ -94,7 +94,7 @@ def test_rebase_path_under_huge_exponents(env, prec):
     eps = 1.25e-3
     got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, prec)
     want = O.softmin(O.SqEuclid(x, z), np.log(b), g, eps)
-    assert _rel(got, want) < (1e-5 if prec == 0 else 1e-7)
+    assert _rel(got, want) < (1e-5 if prec == 0 else 5e-7)
 
 
 def test_deterministic_reruns(env):
