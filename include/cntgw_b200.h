@@ -80,6 +80,24 @@ typedef struct cntgw_sweep_state {
   int32_t pad_;
 } cntgw_sweep_state;
 
+/* Device-resident state of the CNT-GW outer loop (solvers.py:556-625 control)
+ * for the graph-captured solve (cntgw_outer_finish). */
+typedef struct cntgw_outer_state {
+  double constant;       /* loss constant C (divergence.py:41-47)              */
+  double eps_outer;      /* EgwConfig.eps                                       */
+  double delta_outer;    /* EgwConfig.delta_outer                               */
+  double prev_objective; /* objective of the previous outer step               */
+  double t0_ns;          /* %globaltimer at cntgw_outer_init                    */
+  int32_t max_outer;     /* EgwConfig.max_outer                                 */
+  int32_t step;          /* outer steps completed                               */
+  int32_t ups;           /* consecutive objective increases                     */
+  int32_t done;          /* 1: stop (converged, guard tripped or budget used)   */
+  int32_t converged;     /* |dobj| < delta_outer reached                        */
+  int32_t error;         /* 1: divergence guard (SolverError, solvers.py:604)   */
+  int32_t has_prev;
+  int32_t pad_;
+} cntgw_outer_state;
+
 /* ---- library ------------------------------------------------------------ */
 int cntgw_abi_version(void);
 const char* cntgw_last_error(void);
@@ -130,7 +148,9 @@ size_t cntgw_softmin_workspace(int prec, int64_t n, int64_t m, int kd, int sq_fl
 /* out_i = row_add_i - LSE2_j(t_ij)/lam (row_add nullable => 0). If out_max and
  * out_sum are non-null the per-row (max, sum 2^(t-max)) pair is written instead
  * of `out` (partial LSE, finalised after a cross-GPU combine).
- * skip_if_done: return immediately when st->done (graph early exit). */
+ * skip_if_done: 1 = return immediately when st->done (graph early exit);
+ * 2 = return when the loop ended on a symmetrized threshold break (the
+ * tentatives of that sweep are already the final ones). */
 int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int kd, int sq_flag,
                   const void* row_feat, int64_t ld_row, const void* row_sq, const double* row_add,
                   const void* col_rec, int64_t n, int64_t m, double* out, double* out_max,
@@ -185,6 +205,30 @@ int cntgw_outer_reduce_cols(const cntgw_sweep_state* st, const double* g_tilde,
 size_t cntgw_moments_workspace(int64_t n, int d);
 int cntgw_moments(const double* x, int64_t ldx, int d, const double* w, int64_t n, double* out,
                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- device-resident outer loop under CUDA graphs ------------------------- */
+int cntgw_outer_state_size(void);
+int cntgw_outer_init(cntgw_outer_state* os, double constant, double eps_outer, double delta_outer,
+                     int max_outer, void* stream);
+/* Objective, gamma_delta, Err and the stop rule / divergence guard for one
+ * outer step from the K7 reductions (acc_rows = cntgw_outer_reduce_rows output,
+ * acc_cols = cntgw_outer_reduce_cols output); appends one 5-double trace row
+ * [objective, gamma_delta, marginal_err, inner_iters, elapsed_s] at
+ * trace + 5*step; moves gamma -> gamma_prev and Gamma_{t+1} -> gamma (d*e). */
+int cntgw_outer_finish(cntgw_outer_state* os, const cntgw_sweep_state* st, const double* acc_rows,
+                       const double* acc_cols, double* gamma, double* gamma_prev, int de,
+                       double* trace, void* stream);
+/* Stream-capture helpers: begin a capture on `stream` (relaxed mode); open a
+ * conditional WHILE node whose body is captured on `body_stream` until
+ * cntgw_graph_while_end; the body sets its continuation with
+ * cntgw_graph_set_condition (continue while *done_flag == 0). */
+int cntgw_graph_begin(void* stream);
+int cntgw_graph_while_begin(void* stream, void* body_stream, uint64_t* handle_out);
+int cntgw_graph_while_end(void* body_stream);
+int cntgw_graph_set_condition(uint64_t handle, const int32_t* done_flag, void* stream);
+int cntgw_graph_end(void* stream, void** exec_out);
+int cntgw_graph_launch(void* exec, void* stream);
+int cntgw_graph_destroy(void* exec);
 
 #ifdef __cplusplus
 }

@@ -32,6 +32,18 @@ class SweepStateStruct(ctypes.Structure):
     ]
 
 
+class OuterStateStruct(ctypes.Structure):
+    """Host mirror of ``cntgw_outer_state`` (include/cntgw_b200.h)."""
+
+    _fields_ = [
+        ("constant", c_double), ("eps_outer", c_double), ("delta_outer", c_double),
+        ("prev_objective", c_double), ("t0_ns", c_double),
+        ("max_outer", ctypes.c_int32), ("step", ctypes.c_int32), ("ups", ctypes.c_int32),
+        ("done", ctypes.c_int32), ("converged", ctypes.c_int32), ("error", ctypes.c_int32),
+        ("has_prev", ctypes.c_int32), ("pad_", ctypes.c_int32),
+    ]
+
+
 F32, F64, TF32X3 = 0, 1, 2  # cntgw_precision
 
 # name -> (restype, argtypes); every symbol include/cntgw_b200.h declares
@@ -68,6 +80,16 @@ SIGNATURES = {
                                         c_vp]),
     "cntgw_moments_workspace": (c_size_t, [c_i64, c_int]),
     "cntgw_moments": (c_int, [c_vp, c_i64, c_int, c_vp, c_i64, c_vp, c_vp, c_size_t, c_vp]),
+    "cntgw_outer_state_size": (c_int, []),
+    "cntgw_outer_init": (c_int, [c_vp, c_double, c_double, c_double, c_int, c_vp]),
+    "cntgw_outer_finish": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp]),
+    "cntgw_graph_begin": (c_int, [c_vp]),
+    "cntgw_graph_while_begin": (c_int, [c_vp, c_vp, ctypes.POINTER(ctypes.c_uint64)]),
+    "cntgw_graph_while_end": (c_int, [c_vp]),
+    "cntgw_graph_set_condition": (c_int, [ctypes.c_uint64, c_vp, c_vp]),
+    "cntgw_graph_end": (c_int, [c_vp, ctypes.POINTER(c_vp)]),
+    "cntgw_graph_launch": (c_int, [c_vp, c_vp]),
+    "cntgw_graph_destroy": (c_int, [c_vp]),
 }
 
 
@@ -90,6 +112,8 @@ def _load():
         raise ImportError("libcntgw_b200.so ABI version mismatch; rebuild the extension")
     if lib.cntgw_sweep_state_size() != ctypes.sizeof(SweepStateStruct):
         raise ImportError("cntgw_sweep_state layout mismatch between header and host mirror")
+    if lib.cntgw_outer_state_size() != ctypes.sizeof(OuterStateStruct):
+        raise ImportError("cntgw_outer_state layout mismatch between header and host mirror")
     return lib
 
 

@@ -124,8 +124,12 @@ struct TilePipe {
   }
 };
 
-__device__ __forceinline__ bool skip_now(const cntgw_sweep_state* st, int skip_if_done) {
-  return skip_if_done && st != nullptr && st->done;
+// skip modes: 1 = the loop is done; 2 = the loop ended on a symmetrized
+// threshold break (its tentatives are already the final ones)
+__device__ __forceinline__ bool skip_now(const cntgw_sweep_state* st, int skip) {
+  if (!skip || st == nullptr) return false;
+  if (skip == 2) return st->converged && st->threshold > 0.0 && st->mode == 1;
+  return st->done;
 }
 
 __device__ __forceinline__ double block_sum_f64(double v, double* red) {

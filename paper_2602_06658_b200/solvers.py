@@ -24,6 +24,7 @@ with f~ = f - |X_i|^2 and g~ = g - |Gamma Y_j|^2 carried on device.
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass, field, replace
 
@@ -232,6 +233,40 @@ class _GwDevice:
              side.feat64.data_ptr(), 0, self.kd, _stream())
         side.refresh32()
 
+    def set_gamma_dev(self, gamma_dev: torch.Tensor, gamma_t: torch.Tensor):
+        """K5 from a device-resident Gamma (d*e fp64); graph-capturable (no
+        allocation: ``gamma_t`` is a preallocated e x d buffer)."""
+        if self.proj_rows:  # rows: Gamma^T X_i
+            gamma_t.copy_(gamma_dev.view(self.d, self.e).t())
+            op, side, feat, count, din, dout = gamma_t, self.src, self.x, self.n, self.d, self.e
+        else:  # cols: Gamma Y_j
+            op, side, feat, count, din, dout = gamma_dev, self.tgt, self.y, self.m, self.e, self.d
+        call("cntgw_apply_operator", op.data_ptr(), dout, din, feat.data_ptr(), din, count,
+             side.feat64.data_ptr(), 0, self.kd, _stream())
+        side.refresh32()
+
+    def reductions(self, f, g, skip_g: int):
+        """K2 tentative (skipped after a symmetrized threshold break), K4, K7."""
+        st = self.loop.state
+        if self.comm is None:
+            self.bwd(st, f, self.loop.gt, skip=skip_g)
+        self.fwd.pack(st, g, prec=F64)
+        stream = _stream()
+        call("cntgw_plan_reduce", st.ptr, self.kd, self.e, self.src.feat64.data_ptr(), self.kd,
+             self.sx.data_ptr(), f.data_ptr(), self.src.log2w.data_ptr(), self.fwd.rec.data_ptr(),
+             self.y.data_ptr(), self.e, self.ty.data_ptr(), self.n, self.m, self.r.data_ptr(),
+             self.pi_y.data_ptr(), self.pi_s.data_ptr(), self.argmax.data_ptr(),
+             self.ws_plan.data_ptr(), self.ws_plan.numel(), stream)
+        nrow = 16 + self.d * self.e
+        call("cntgw_outer_reduce_rows", self.x.data_ptr(), self.d, self.d, self.pi_y.data_ptr(),
+             self.e, self.r.data_ptr(), self.pi_s.data_ptr(), f.data_ptr(), self.sx.data_ptr(),
+             self.a.data_ptr(), self.n, self.acc.data_ptr(), self.ws_outer.data_ptr(),
+             self.ws_outer.numel(), stream)
+        call("cntgw_outer_reduce_cols", st.ptr, g.data_ptr(), self.loop.gt.data_ptr(),
+             self.ty.data_ptr(), self.b.data_ptr(), self.m, self.acc[nrow:].data_ptr(),
+             self.ws_outer.data_ptr(), self.ws_outer.numel(), stream)
+        return nrow
+
     def col_sep(self, gamma) -> torch.Tensor:
         """|Gamma Y_j|^2 in fp64 (reference separable column part)."""
         g = torch.as_tensor(np.ascontiguousarray(gamma, dtype=np.float64), device=self.device)
@@ -412,6 +447,120 @@ class _CntGwState:
         )
 
 
+class _DeviceSolve:
+    """The whole outer loop as ONE CUDA graph (single GPU).
+
+    Captured once: an outer conditional WHILE node whose body is K5 (operator
+    from the device-resident Gamma), the Sinkhorn loop (n_inner sweeps, or an
+    inner conditional WHILE node that exits on the device-side threshold
+    decision), the final tentative, K4/K7 and ``cntgw_outer_finish`` (objective,
+    trace row, stop rule and divergence guard on the device), which sets the
+    outer condition. The host launches it once and reads the trace at the end.
+    """
+
+    def __init__(self, state: "_CntGwState"):
+        import ctypes
+
+        from ._native import OuterStateStruct
+
+        self.state = state
+        dev, cfg = state.dev, state.cfg
+        self.loop_cfg = cfg.inner.with_temperature(cfg.eps / 8.0).loop_config()
+        device = state.device
+        self.gamma = torch.as_tensor(np.ascontiguousarray(state.gamma).ravel(), device=device).clone()
+        self.gamma_prev = torch.zeros_like(self.gamma)
+        self.gamma_t = torch.zeros(dev.e * dev.d, dtype=torch.float64, device=device)
+        self.trace = torch.zeros(5 * cfg.max_outer, dtype=torch.float64, device=device)
+        self.os = torch.zeros(ctypes.sizeof(OuterStateStruct), dtype=torch.uint8, device=device)
+        self._struct = OuterStateStruct
+        # features and precision for the first step, fixed for the captured solve
+        dev.set_gamma(state.gamma)
+        dev.choose_precision(state.f, state.g, self.loop_cfg.eps)
+        self.exec = None
+
+    def _capture(self):
+        st, dev, cfg, lc = self.state, self.state.dev, self.state.cfg, self.loop_cfg
+        loop = dev.loop
+        s0, s1, s2 = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        s0.wait_stream(torch.cuda.current_stream())
+        import ctypes
+
+        h1, h2 = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        done_sweep = loop.state.ptr + _native_offset("done")
+        done_outer = self.os.data_ptr() + self._struct.done.offset
+        with torch.cuda.stream(s0):
+            call("cntgw_graph_begin", s0.cuda_stream)
+            call("cntgw_outer_init", self.os.data_ptr(), float(st.constant), float(cfg.eps),
+                 float(cfg.delta_outer), int(cfg.max_outer), s0.cuda_stream)
+            call("cntgw_graph_while_begin", s0.cuda_stream, s1.cuda_stream, ctypes.byref(h1))
+            with torch.cuda.stream(s1):
+                dev.set_gamma_dev(self.gamma, self.gamma_t)
+                loop.state.init(lc.eps, lc.anneal_from, lc.threshold, lc.max_sweeps, lc.mode)
+                if lc.threshold is None:
+                    for _ in range(lc.max_sweeps):
+                        loop.sweep(st.f, st.g, lc.mode)
+                else:
+                    call("cntgw_graph_while_begin", s1.cuda_stream, s2.cuda_stream, ctypes.byref(h2))
+                    with torch.cuda.stream(s2):
+                        loop.sweep(st.f, st.g, lc.mode)
+                        call("cntgw_graph_set_condition", h2.value, done_sweep, s2.cuda_stream)
+                    call("cntgw_graph_while_end", s2.cuda_stream)
+                loop.state.begin()  # a fully used budget is marked done
+                nrow = dev.reductions(st.f, st.g, skip_g=2)
+                call("cntgw_outer_finish", self.os.data_ptr(), loop.state.ptr, dev.acc.data_ptr(),
+                     dev.acc[nrow:].data_ptr(), self.gamma.data_ptr(), self.gamma_prev.data_ptr(),
+                     dev.d * dev.e, self.trace.data_ptr(), s1.cuda_stream)
+                call("cntgw_graph_set_condition", h1.value, done_outer, s1.cuda_stream)
+            call("cntgw_graph_while_end", s1.cuda_stream)
+            exec_ptr = ctypes.c_void_p()
+            call("cntgw_graph_end", s0.cuda_stream, ctypes.byref(exec_ptr))
+        self.exec = exec_ptr.value
+        self.stream = s0
+
+    def run(self):
+        """Launch the captured solve; returns (trace rows, converged, error)."""
+        self._capture()
+        try:
+            call("cntgw_graph_launch", self.exec, self.stream.cuda_stream)
+            self.stream.synchronize()
+        finally:
+            call("cntgw_graph_destroy", self.exec)
+        torch.cuda.current_stream().wait_stream(self.stream)
+        os_ = self._struct.from_buffer_copy(self.os.cpu().numpy().tobytes())
+        rows = self.trace.view(-1, 5)[: os_.step].cpu().numpy()
+        st, dev = self.state, self.state.dev
+        st.gamma = self.gamma.view(dev.d, dev.e).cpu().numpy().copy()
+        st.coupling_gamma = self.gamma_prev.view(dev.d, dev.e).cpu().numpy().copy()
+        st.eps_eff = float(dev.loop.state.read().eps_n)
+        return rows, bool(os_.converged), bool(os_.error)
+
+
+def _native_offset(field: str) -> int:
+    from ._native import SweepStateStruct
+
+    return getattr(SweepStateStruct, field).offset
+
+
+def _run_outer_device(state, cfg: EgwConfig) -> EgwResult:
+    """Graph-captured outer loop (same semantics as _run_outer, single GPU)."""
+    rows, converged, error = _DeviceSolve(state).run()
+    if error:
+        raise SolverError(
+            f"objective increased {_DIVERGENCE_PATIENCE} outer steps in a "
+            "row; raise n_inner or use the adaptive wrapper"
+        )
+    trace = SolveTrace()
+    for k, (obj, delta, err, iters, t) in enumerate(rows, start=1):
+        trace.append(k, obj, delta, err, int(iters), t)
+    if cfg.final_anneal is not None:
+        t0 = time.perf_counter()
+        stats = state.step(anneal_from=cfg.final_anneal)
+        last = trace.elapsed_s[-1] if len(trace) else 0.0
+        trace.append(len(trace) + 1, stats.objective, stats.gamma_delta, stats.marginal_err,
+                     stats.inner_iters, last + time.perf_counter() - t0)
+    return state.result(trace, converged)
+
+
 def _run_outer(state, cfg: EgwConfig, adaptive: bool = False) -> EgwResult:
     """Outer control: trace, |dobj| stop, 5-increase guard, adaptive doubling,
     optional final annealed step (reference solvers.py:556-625)."""
@@ -464,8 +613,18 @@ def _run_outer(state, cfg: EgwConfig, adaptive: bool = False) -> EgwResult:
 
 
 def solve_cnt_gw(src, tgt, cfg: EgwConfig, _warm_potentials=None) -> EgwResult:
-    """Feature-space EGW solve (reference solvers.py:628-632)."""
-    return _run_outer(_CntGwState(src, tgt, cfg, warm_potentials=_warm_potentials), cfg)
+    """Feature-space EGW solve (reference solvers.py:628-632).
+
+    On one GPU the whole outer loop runs as a single CUDA graph
+    (``_DeviceSolve``); row-sharded multi-GPU runs and ``record_iterates``
+    use the host-driven loop over the same device kernels. Set
+    CNTGW_DEVICE_LOOP=0 to force the host-driven loop.
+    """
+    state = _CntGwState(src, tgt, cfg, warm_potentials=_warm_potentials)
+    if (state.dev.comm is None and not cfg.record_iterates
+            and os.environ.get("CNTGW_DEVICE_LOOP", "1") != "0"):
+        return _run_outer_device(state, cfg)
+    return _run_outer(state, cfg)
 
 
 def solve_adaptive(solver, *args, cfg: EgwConfig) -> EgwResult:
