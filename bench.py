@@ -49,9 +49,12 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--n", type=int, default=C2["n"], help="override N=M (smoke runs)")
+    p.add_argument("--size", type=int, default=C2["n"], help="override N=M (smoke runs)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--backend", default=None, choices=[None, "nccl", "gloo"],
+                   help="collective backend under torchrun (default nccl; gloo only for "
+                        "single-GPU functional checks of the multi-rank path)")
     return p.parse_args()
 
 
@@ -153,7 +156,7 @@ def run_reference(args, info):
 
     if info.rank != 0:
         return
-    n = args.n
+    n = args.size
     inst = configs.c2(seed=C2["seed"], n=n, k=C2["k"])
     threads = os.cpu_count() or 1
     rates = []
@@ -189,9 +192,11 @@ def run_b200(args, info):
     from paper_2602_06658_b200 import configs, dist, engine
     from paper_2602_06658_b200._native import F32, F64, TF32X3
 
-    dev = engine.require_cuda(info.local_rank)
+    # CNTGW_BENCH_DEVICE pins every rank to one device (functional checks of the
+    # multi-rank path on a 1-GPU box with --backend gloo; never for timing)
+    dev = engine.require_cuda(int(os.environ.get("CNTGW_BENCH_DEVICE", info.local_rank)))
     torch.cuda.set_device(dev)
-    n = m = args.n
+    n = m = args.size
     k = C2["k"]
     inst = configs.c2(seed=C2["seed"], n=n, m=m, k=k)
     lo, hi = dist.shard_range(n, info.rank, info.world)
@@ -335,6 +340,8 @@ def run_b200(args, info):
         roof, bound = min(peaks["ex2_per_s"], peaks["ffma_per_s"] / fma_ops), "fma"
         model = f"min(MUFU.EX2/s, FFMA/s / {fma_ops}) per pair (K={k} dot + 2)"
     clk = clocks.summary()
+    kernel_tag = {F32: "softmin_f32_kernel", F64: "softmin_f64_kernel", TF32X3: "softmin_tc_kernel"}
+    traffic = ncu_traffic(kernel_tag[prec], n, m)
     line = {
         "metric": "softmin_pairs_per_s", "value": value, "unit": "pairs/s", "n_gpus": info.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -344,7 +351,7 @@ def run_b200(args, info):
                    "n": n, "m": m, "k": k, "eps": C2["eps"], "parallelism": f"rows sharded x{info.world}",
                    "l2": "flushed by a 256 MiB write before every timed step"},
         "roofline": {"bound": bound, "achieved": achieved, "peak": roof, "unit": "pairs/s",
-                     "frac": achieved / roof, "traffic": None, "path": path, "model": model,
+                     "frac": achieved / roof, "traffic": traffic, "path": path, "model": model,
                      "peak_source": peaks["source"], "kernel_avg_ms": kern_avg_ms,
                      "pairs_per_launch": nl * m},
         "e2e": e2e,
@@ -360,6 +367,24 @@ def run_b200(args, info):
     print(json.dumps(line), flush=True)
 
 
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r1_bench_traffic.json")
+
+
+def ncu_traffic(tag, n, m):
+    """DRAM bytes per launch of the dominant kernel from the committed
+    `ncu --set full` capture of this same bench command (profiles/), or None
+    when no capture of this workload size exists."""
+    if not os.path.exists(TRAFFIC_FILE):
+        return None
+    data = json.load(open(TRAFFIC_FILE))
+    if data.get("_workload") != {"n": n, "m": m}:
+        return None
+    for name, rec in data.items():
+        if tag in name and isinstance(rec, dict) and "dram_bytes_per_launch" in rec:
+            return rec["dram_bytes_per_launch"]
+    return None
+
+
 def main():
     args = parse()
     from paper_2602_06658_b200 import dist
@@ -370,7 +395,11 @@ def main():
                              world=int(os.environ.get("WORLD_SIZE", "1")))
         run_reference(args, info)
         return
-    info = dist.init_from_env()
+    if args.backend == "gloo" and "CNTGW_BENCH_DEVICE" in os.environ:
+        import torch
+
+        torch.cuda.set_device(int(os.environ["CNTGW_BENCH_DEVICE"]))
+    info = dist.init_from_env(args.backend)
     run_b200(args, info)
     if info.enabled:
         import torch.distributed as tdist

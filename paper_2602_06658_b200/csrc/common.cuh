@@ -57,6 +57,33 @@ __device__ __forceinline__ float f64_to_f32_fast(double w) {
   return __uint_as_float((f & 0x7fffffffu) | (hi & 0x80000000u));
 }
 
+// float -> double with integer ops (exact for normal v >= 0; 0 and subnormals
+// -> 0): F2F.F64.F32 would queue on the XU pipe behind the MUFU.EX2 stream
+// of the streaming kernels and stall the warp at every tile end.
+__device__ __forceinline__ double f32_to_f64_alu(float v) {
+  const uint32_t u = __float_as_uint(v);
+  const uint32_t hi = u >= 0x00800000u ? (u >> 3) + (896u << 20) : 0u;
+  return __hiloint2double((int)hi, (int)(hi ? u << 29 : 0u));
+}
+
+// Float-float running sum (hi + lo, ~44-bit significand) on the FMA pipe: the
+// epilogue of the tcgen05 kernel folds one fp32 tile sum per row per tile, and
+// a DADD there stalls on math-pipe throttle behind the MUFU.EX2 stream.
+struct FFSum {
+  float hi = 0.f, lo = 0.f;
+  __device__ __forceinline__ void add(float t) {  // Knuth TwoSum
+    const float s = hi + t;
+    const float bp = s - hi;
+    lo += (hi - (s - bp)) + (t - bp);
+    hi = s;
+  }
+  __device__ __forceinline__ void scale(float c) {
+    hi *= c;
+    lo *= c;
+  }
+  __device__ __forceinline__ double value() const { return (double)hi + (double)lo; }
+};
+
 // Packed fp32x2 arithmetic (sm_100a FFMA2/FADD2): two rows per instruction.
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
   float2 d;

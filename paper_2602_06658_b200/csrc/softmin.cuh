@@ -83,6 +83,11 @@ __device__ __forceinline__ void softmin_tile_f32(const float* __restrict__ rec,
                                                  double (&S)[R]) {
   using L = ColLayout<float, KD, SQ>;
   constexpr int P = R / 2;
+  // per-tile fp32 sums (row pairs), folded into the fp64 S once per tile so no
+  // F2F.F64 conversion (an XU-pipe op, shared with MUFU.EX2) runs per group
+  float2 T[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) T[p] = f2(0.f, 0.f);
 #pragma unroll 1
   for (int j = 0; j < TILE; j += G) {
     float2 q[P][G];
@@ -119,25 +124,35 @@ __device__ __forceinline__ void softmin_tile_f32(const float* __restrict__ rec,
         const float2 v = fma2(q[p][g], f2(-1.f, -1.f), m2);
         gs = add2(gs, f2(ex2(v.x), ex2(v.y)));
       }
+      if (!(gs.x <= kRebase) || !(gs.y <= kRebase)) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = 2 * p + h;
-        float gsum = h ? gs.y : gs.x;
-        if (!(gsum <= kRebase)) {  // rare: rebase the row reference at the group minimum
-          float qmin = h ? q[p][0].y : q[p][0].x;
+        for (int h = 0; h < 2; ++h) {  // rare: rebase the row reference at the group minimum
+          const int r = 2 * p + h;
+          float gsum = h ? gs.y : gs.x;
+          if (!(gsum <= kRebase)) {
+            float qmin = h ? q[p][0].y : q[p][0].x;
 #pragma unroll
-          for (int g = 1; g < G; ++g) qmin = fminf(qmin, h ? q[p][g].y : q[p][g].x);
-          if (qmin < mq[r]) {
-            S[r] *= (double)ex2(qmin - mq[r]);
-            mq[r] = qmin;
+            for (int g = 1; g < G; ++g) qmin = fminf(qmin, h ? q[p][g].y : q[p][g].x);
+            if (qmin < mq[r]) {
+              const float sc = ex2(qmin - mq[r]);
+              S[r] *= (double)sc;
+              if (h) T[p].y *= sc; else T[p].x *= sc;
+              mq[r] = qmin;
+            }
+            gsum = 0.f;
+#pragma unroll
+            for (int g = 0; g < G; ++g) gsum += ex2(mq[r] - (h ? q[p][g].y : q[p][g].x));
+            if (h) gs.y = gsum; else gs.x = gsum;
           }
-          gsum = 0.f;
-#pragma unroll
-          for (int g = 0; g < G; ++g) gsum += ex2(mq[r] - (h ? q[p][g].y : q[p][g].x));
         }
-        S[r] += (double)gsum;
       }
+      T[p] = add2(T[p], gs);
     }
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    S[2 * p] += f32_to_f64_alu(T[p].x);
+    S[2 * p + 1] += f32_to_f64_alu(T[p].y);
   }
 }
 
@@ -219,6 +234,9 @@ __device__ __forceinline__ void softmin_tile_f64(const double* __restrict__ rec,
                                                  const double (&x)[R][KD], const double (&s)[R],
                                                  double (&mq)[R], double (&S)[R]) {
   using L = ColLayout<double, KD, SQ>;
+  float T[R];  // per-tile fp32 sums, folded into S once per tile (no per-group F2F)
+#pragma unroll
+  for (int r = 0; r < R; ++r) T[r] = 0.f;
 #pragma unroll 1
   for (int j = 0; j < TILE; j += G) {
     double q[R][G];
@@ -254,16 +272,20 @@ __device__ __forceinline__ void softmin_tile_f64(const double* __restrict__ rec,
         for (int g = 1; g < G; ++g) qmin = fmin(qmin, q[r][g]);
         const double ref = qmin + kRefOffset;
         if (ref < mq[r]) {
-          S[r] *= exp2(ref - mq[r]);
+          const double sc = exp2(ref - mq[r]);
+          S[r] *= sc;
+          T[r] *= (float)sc;
           mq[r] = ref;
         }
         gsum = 0.f;
 #pragma unroll
         for (int g = 0; g < G; ++g) gsum += ex2(f64_to_f32_fast(mq[r] - q[r][g]));
       }
-      S[r] += (double)gsum;
+      T[r] += gsum;
     }
   }
+#pragma unroll
+  for (int r = 0; r < R; ++r) S[r] += f32_to_f64_alu(T[r]);
 }
 
 template <int KD, int SQ, int R, int G, int MINB, int TILE>

@@ -13,7 +13,10 @@
 //
 // Warp roles (one CTA per SM, 128 rows x one column chunk):
 //   warp 0      TMA producer: 1-D bulk copies of prepacked B' tiles (56 KB for
-//               KD=16) into a 2-stage shared-memory ring (mbarrier full/empty)
+//               KD=16) into a kTcStages-deep shared-memory ring (mbarrier
+//               full/empty); three stages keep two tiles of L2/DRAM latency
+//               in flight ahead of the MMA (the whole 2^20-column B' set,
+//               235 MB, does not fit the 126 MB L2)
 //   warp 1      TMEM allocator + MMA issuer: one elected lane issues
 //               tcgen05.mma.kind::tf32 (M=128, N=256, K=8 per instruction) and
 //               tcgen05.commit to release the smem stage and publish the tile
@@ -32,6 +35,7 @@ namespace cntgw {
 
 constexpr int kTcRows = 128;   // rows per CTA (= TMEM lanes)
 constexpr int kTcCols = 256;   // columns per tile (= MMA N)
+constexpr int kTcStages = 3;   // B' shared-memory ring depth
 // producer + MMA warps + EPI epilogue warps (EPI/4 per TMEM lane quadrant)
 constexpr int tc_threads(int epi) { return 64 + 32 * epi; }
 
@@ -164,7 +168,7 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
 // on the FMA pipe and the rest on MUFU.EX2; a chunk whose sum leaves [0, 2^20]
 // (or is inf/NaN) rebases the row reference at the chunk maximum.
 template <int NPOLY>
-__device__ __forceinline__ void tc_chunk(const float (&v)[32], float& mref, float& tsum, double& S) {
+__device__ __forceinline__ void tc_chunk(const float (&v)[32], float& mref, float& tsum, FFSum& S) {
   float2 nm = f2(-mref, -mref);
   float2 acc[4] = {f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f)};
 #pragma unroll
@@ -186,7 +190,7 @@ __device__ __forceinline__ void tc_chunk(const float (&v)[32], float& mref, floa
     for (int u = 1; u < 32; ++u) cm = fmaxf(cm, v[u]);
     if (cm > mref) {
       const float sc = ex2(mref - cm);
-      S *= (double)sc;
+      S.scale(sc);
       tsum *= sc;
       mref = cm;
     }
@@ -206,7 +210,7 @@ template <int KD, int NPOLY, int EPI>
 __global__ void __launch_bounds__(tc_threads(EPI), 1) softmin_tc_kernel(const SoftminArgs a) {
   using L = TcLayout<KD>;
   extern __shared__ __align__(1024) float smem_tc[];
-  __shared__ uint64_t full_bar[2], empty_bar[2], tfull_bar[2], tempty_bar[2];
+  __shared__ uint64_t full_bar[kTcStages], empty_bar[kTcStages], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
   constexpr int kParts = EPI / 4;                  // column parts per TMEM quadrant
   constexpr int kChunksPerPart = kTcCols / kParts / 32;
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(tc_threads(EPI), 1) softmin_tc_kernel(const So
   if (skip_now(a.st, a.skip)) return;
 
   float* sA = smem_tc;                       // A' : kChunks x 128 rows x 16 B
-  float* sB = smem_tc + L::kATileFloats;     // B' : 2 stages
+  float* sB = smem_tc + L::kATileFloats;     // B' : kTcStages stages
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int chunk = blockIdx.y;
   const int64_t row0 = (int64_t)blockIdx.x * kTcRows;
@@ -224,9 +228,11 @@ __global__ void __launch_bounds__(tc_threads(EPI), 1) softmin_tc_kernel(const So
   const int ntiles = (int)((min(c0 + a.chunk_cols, mpad) - c0) / kTcCols);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kTcStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], EPI);
     }
@@ -267,38 +273,39 @@ __global__ void __launch_bounds__(tc_threads(EPI), 1) softmin_tc_kernel(const So
     if (lane == 0) {  // producer
       const uint32_t bytes = L::kBTileFloats * sizeof(float);
       const float* src = static_cast<const float*>(a.col_rec) + (c0 / kTcCols) * L::kBTileFloats;
-      for (int t = 0; t < ntiles; ++t) {
-        const int s = t & 1;
-        mbar_wait(&empty_bar[s], ((t >> 1) & 1) ^ 1);
+      for (int t = 0, s = 0, ph = 0; t < ntiles; ++t) {
+        mbar_wait(&empty_bar[s], ph ^ 1);
         mbar_expect_tx(&full_bar[s], bytes);
         bulk_g2s(sB + s * L::kBTileFloats, src + (int64_t)t * L::kBTileFloats, bytes, &full_bar[s]);
+        if (++s == kTcStages) s = 0, ph ^= 1;
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       const uint32_t a0 = smem_u32(sA);
-      for (int t = 0; t < ntiles; ++t) {
-        const int s = t & 1;
-        mbar_wait(&full_bar[s], (t >> 1) & 1);
-        mbar_wait(&tempty_bar[s], ((t >> 1) & 1) ^ 1);
+      for (int t = 0, s = 0, ph = 0; t < ntiles; ++t) {
+        const int ab = t & 1;  // TMEM accumulator buffer
+        mbar_wait(&full_bar[s], ph);
+        mbar_wait(&tempty_bar[ab], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t b0 = smem_u32(sB + s * L::kBTileFloats);
-        const uint32_t d = tmem + (uint32_t)(s * kTcCols);
+        const uint32_t d = tmem + (uint32_t)(ab * kTcCols);
 #pragma unroll
         for (int ks = 0; ks < L::kKp / 8; ++ks) {
           const uint64_t ad = umma_desc(a0 + ks * 2 * (kTcRows * 16), kTcRows * 16, 128);
           const uint64_t bd = umma_desc(b0 + ks * 2 * (kTcCols * 16), kTcCols * 16, 128);
           tc_mma(d, ad, bd, ks > 0 ? 1u : 0u);
         }
-        tc_commit(&empty_bar[s]);  // smem stage reusable once these MMAs completed
-        tc_commit(&tfull_bar[s]);  // accumulator s ready for the epilogue
+        tc_commit(&empty_bar[s]);   // smem stage reusable once these MMAs completed
+        tc_commit(&tfull_bar[ab]);  // accumulator ab ready for the epilogue
+        if (++s == kTcStages) s = 0, ph ^= 1;
       }
     }
   } else {  // epilogue warps
     const int q = warp & 3;             // TMEM lane quadrant (rows 32q..32q+31)
     const int part = (warp - 2) >> 2;   // column part of each tile
     float mref = -CUDART_INF_F;         // lazily rebased row reference (log2 units)
-    double S = 0.0;                     // sum over finished tiles of 2^(t - mref)
+    FFSum S;                                    // sum over finished tiles of 2^(t - mref)
     float va[32], vb[32];
     for (int t = 0; t < ntiles; ++t) {
       const int s = t & 1;
@@ -323,12 +330,12 @@ __global__ void __launch_bounds__(tc_threads(EPI), 1) softmin_tc_kernel(const So
         tc_chunk<NPOLY>(cur, mref, tsum, S);
         if (c + 1 < kChunksPerPart) tmem_wait_ld();
       }
-      S += (double)tsum;
+      S.add(tsum);
     }
     // merge the column parts of each row, then store
     const int r = 32 * q + lane;
     red_m[part][r] = mref;
-    red_s[part][r] = S;
+    red_s[part][r] = S.value();
     asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI) : "memory");  // epilogue warps only
     if (part == 0) {
       float mm = red_m[0][r];

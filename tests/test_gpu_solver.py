@@ -141,3 +141,40 @@ def test_law_trajectory(P, name, eps, n_inner):
     if int(gold["raise_at"]) > 0:
         with pytest.raises(P.SolverError):
             P.solve_cnt_gw(src, tgt, cfg)
+
+
+def test_device_graph_loop_equals_host_loop(P, monkeypatch):
+    """The single-graph solve (nested conditional WHILE nodes) and the
+    host-driven loop run the same kernels: identical trajectories."""
+    gold = golden("c1_solve")
+    src, tgt = _measures(P, gold)
+    cfg = P.make_config(0.01, threshold=1e-5, max_inner=200, max_outer=20)
+    dev_res = P.solve_cnt_gw(src, tgt, cfg)
+    monkeypatch.setenv("CNTGW_DEVICE_LOOP", "0")
+    host_res = P.solve_cnt_gw(src, tgt, cfg)
+    assert dev_res.trace.inner_iters == host_res.trace.inner_iters
+    # the objective is summed on the device in one loop and on the host in
+    # another: equal to the last couple of ulps
+    np.testing.assert_allclose(dev_res.trace.objectives, host_res.trace.objectives, rtol=1e-13)
+    assert np.array_equal(dev_res.coupling.f, host_res.coupling.f)
+    assert np.array_equal(dev_res.gamma, host_res.gamma)
+    assert np.array_equal(dev_res.argmax, host_res.argmax)
+    assert all(t > 0 for t in dev_res.trace.elapsed_s)
+
+
+def test_final_anneal_and_fixed_budget_graph(P):
+    """final_anneal appends one annealed step after the captured loop."""
+    gold = golden("c1_solve")
+    src, tgt = _measures(P, gold)
+    cfg = P.make_config(0.01, n_inner=8, max_outer=3, final_anneal=0.05, delta_outer=1e-12)
+    res = P.solve_cnt_gw(src, tgt, cfg)
+    assert len(res.trace) == 4 and res.trace.inner_iters == [8, 8, 8, 8]
+    from oracle import cntgw_oracle as O
+
+    ref = O.solve_cnt_gw(gold["x_feat"], gold["a"], gold["y_feat"], gold["b"], 0.01,
+                         dict(n_inner=8), max_outer=3, delta_outer=1e-12, final_anneal=0.05)
+    # a fixed 8-sweep budget stops the annealing schedule before eps' = eps/8
+    assert res.coupling.eps_eff == pytest.approx(ref["eps_eff"], rel=1e-12)
+    assert res.coupling.eps_eff > 0.01 / 8
+    assert _rel(res.trace.objectives, ref["trace"]["objective"]) < TOL
+    assert _rel(res.coupling.f, ref["f"]) < TOL

@@ -1,8 +1,11 @@
 """Summarise an ncu report: pipe utilisation, stalls, occupancy, DRAM traffic.
-Usage: python tools/ncu_summary.py report.ncu-rep [launches.csv]"""
+Usage: python tools/ncu_summary.py report.ncu-rep [launches.csv]
+       python tools/ncu_summary.py --traffic-json out.json report.ncu-rep N M
+  (per-kernel DRAM bytes per launch, read by bench.py for roofline.traffic)"""
 import collections
 import csv
 import io
+import json
 import subprocess
 import sys
 
@@ -60,5 +63,25 @@ def main(rep, launches=None):
             print(f"  {v[1] / tot * 100:6.2f}%  n={v[0]:3d}  {v[1] / 1e6:9.3f} ms  {k}")
 
 
+_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def traffic_json(out, rep, n, m):
+    res = {"_workload": {"n": int(n), "m": int(m)}}
+    for rec in raw(rep):
+        name = rec["Kernel Name"][0]
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            v, u = rec[k]
+            tot += float(v.replace(",", "")) * _SCALE[u]
+        res[name] = {"dram_bytes_per_launch": tot, "report": rep.split("/")[-1],
+                     "grid": rec["launch__grid_size"][0], "block": rec["launch__block_size"][0]}
+    json.dump(res, open(out, "w"), indent=1)
+    print(json.dumps(res, indent=1))
+
+
 if __name__ == "__main__":
-    main(*sys.argv[1:])
+    if sys.argv[1] == "--traffic-json":
+        traffic_json(*sys.argv[2:6])
+    else:
+        main(*sys.argv[1:])

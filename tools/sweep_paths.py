@@ -55,13 +55,17 @@ def main(n=1 << 19, reps=3, rounds=3, only=None):
     dev = torch.device("cuda", 0)
     variants = []
     src, tgt, eps, pot = build(n, 16, False)
-    for prec, poly, epi in [(F32, 0, 8), (TF32X3, 0, 8), (TF32X3, 2, 8), (TF32X3, 4, 8), (TF32X3, 6, 8),
-                            (TF32X3, 0, 16), (TF32X3, 2, 16)]:
-        variants.append((f"C2 K=16 prec={prec} poly={poly} epi={epi}", src, tgt, eps, pot, prec,
-                         {"CNTGW_TC_POLY": str(poly), "CNTGW_TC_EPI": str(epi)}))
+    for prec, poly, epi, l2 in [(F32, 0, 8, 32), (TF32X3, 0, 16, 0), (TF32X3, 0, 16, 32),
+                                (TF32X3, 2, 8, 32), (TF32X3, 2, 16, 32), (TF32X3, 4, 16, 32),
+                                (TF32X3, 6, 16, 32)]:
+        variants.append((f"C2 K=16 prec={prec} poly={poly} epi={epi} l2={l2}", src, tgt, eps, pot, prec,
+                         {"CNTGW_TC_POLY": str(poly), "CNTGW_TC_EPI": str(epi),
+                          "CNTGW_L2_CHUNK_MB": str(l2)}))
     s4, t4, e4, p4 = build(n, 3, True)
-    for prec in (F32, F64):
-        variants.append((f"C4-law K=3+sq prec={prec}", s4, t4, e4, p4, prec, {}))
+    variants.append((f"C4-law K=3+sq prec={F32}", s4, t4, e4, p4, F32, {"CNTGW_L2_CHUNK_MB": "32"}))
+    for rg, l2 in (("0", 32), ("0", 0), ("44", 32), ("24", 32)):
+        variants.append((f"C4-law K=3+sq prec={F64} rg={rg} l2={l2}", s4, t4, e4, p4, F64,
+                         {"CNTGW_F64_RG": rg, "CNTGW_L2_CHUNK_MB": str(l2)}))
     if only:
         variants = [v for v in variants if all(tok in v[0] for tok in only.split(","))]
     results = {v[0]: [] for v in variants}
