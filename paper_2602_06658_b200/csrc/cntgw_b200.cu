@@ -8,6 +8,7 @@
 
 #include "common.cuh"
 #include "softmin.cuh"
+#include "softmin_dmma.cuh"
 #include "softmin_tc.cuh"
 #include "sweep.cuh"
 
@@ -91,6 +92,7 @@ struct KernelPick {
   size_t smem;
   int threads = 128;
   size_t rec_bytes = 0;  // bytes of column records per column (L2 chunking)
+  int cta_rows = 0;      // rows per CTA when not 128 * rows
 };
 
 template <int PREC, int KD, int SQ>
@@ -108,13 +110,12 @@ KernelPick pick() {
     k.rows = rows_f64<KD>();
     k.smem = 2 * (size_t)T * ColLayout<double, KD, SQ>::kStride * sizeof(double);
     k.rec_bytes = ColLayout<double, KD, SQ>::kStride * sizeof(double);
-    if constexpr (KD <= 4) {  // tuning variants for the small-K fp64 path (CNTGW_F64_RG = R*10+G)
-      switch (env_int("CNTGW_F64_RG", 0)) {
-        case 24: k.fn = (void*)softmin_f64_kernel<KD, SQ, 2, 4, 8, T>; k.rows = 2; break;
-        case 44: k.fn = (void*)softmin_f64_kernel<KD, SQ, 4, 4, 4, T>; k.rows = 4; break;
-        case 82: k.fn = (void*)softmin_f64_kernel<KD, SQ, 8, 2, 3, T>; k.rows = 8; break;
-        case 84: k.fn = (void*)softmin_f64_kernel<KD, SQ, 8, 4, 2, T>; k.rows = 8; break;
-        default: break;
+    if constexpr (KD >= 16) {  // wide features: the dot on the FP64 tensor pipe (DMMA)
+      if (env_int("CNTGW_F64_DMMA", 1)) {
+        constexpr int RG = KD >= 64 ? 2 : 4, TD = KD >= 64 ? 64 : 128;
+        k.fn = (void*)softmin_dmma_kernel<KD, SQ, RG, TD, 3>;
+        k.cta_rows = 32 * RG;
+        k.smem = 2 * (size_t)TD * ColLayout<double, KD, SQ>::kStride * sizeof(double);
       }
     }
   }
@@ -179,7 +180,7 @@ struct Plan {
 // whole waves of the resident-CTA capacity (tail < 3% when possible).
 Plan plan_softmin(int64_t n, int64_t m, const KernelPick& k) {
   Plan p;
-  const int64_t rows_per_cta = 128LL * k.rows;
+  const int64_t rows_per_cta = k.cta_rows > 0 ? k.cta_rows : 128LL * k.rows;
   p.row_tiles = (int)((n + rows_per_cta - 1) / rows_per_cta);
   const int64_t tiles = (m + kColTile - 1) / kColTile;
   int occ = 1;
@@ -303,7 +304,7 @@ int cntgw_col_stride(int prec, int kd, int sq) {
   if (!kd_supported(kd)) return fail(CNTGW_EINVAL, "unsupported feature width kd=%d", kd);
   const int raw = kd + (sq ? 1 : 0) + 1;
   if (prec == CNTGW_F32) return (raw + 3) / 4 * 4;
-  if (prec == CNTGW_F64) return (raw + 1) / 2 * 2;
+  if (prec == CNTGW_F64) return kd >= 16 ? (raw + 3) / 4 * 4 : (raw + 1) / 2 * 2;
   if (prec == CNTGW_TF32X3) {
     if (sq || (kd != 8 && kd != 16))
       return fail(CNTGW_EINVAL, "tensor-core path supports kd in {8,16} without sq (kd=%d sq=%d)", kd, sq);

@@ -54,7 +54,11 @@ __device__ __forceinline__ float f64_to_f32_fast(double w) {
   const uint32_t lo = (uint32_t)__double2loint(w);
   const uint32_t hi = (uint32_t)__double2hiint(w);
   const uint32_t f = __funnelshift_l(lo, hi - 0x38000000u, 3);
-  return __uint_as_float((f & 0x7fffffffu) | (hi & 0x80000000u));
+  // (f & 0x7fffffff) | (hi & 0x80000000) as ONE bit-select LOP3 (LUT 0xE2:
+  // a&b | c&~b); the compiler otherwise emits two
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(r) : "r"(f), "n"(0x7fffffff), "r"(hi));
+  return __uint_as_float(r);
 }
 
 // float -> double with integer ops (exact for normal v >= 0; 0 and subnormals

@@ -54,7 +54,9 @@ template <typename T, int KD, int SQ>
 struct ColLayout {
   static constexpr int kRaw = KD + SQ + 1;
   static constexpr int kPerVec = 16 / sizeof(T);                        // elements per 16 B
-  static constexpr int kStride = (kRaw + kPerVec - 1) / kPerVec * kPerVec;  // elements
+  // elements; fp64 records of wide features are padded to the DMMA k4 step
+  static constexpr int kStride = (sizeof(T) == 8 && KD >= 16) ? (kRaw + 3) / 4 * 4
+                                                              : (kRaw + kPerVec - 1) / kPerVec * kPerVec;
   static constexpr int kBeta = KD + SQ;                                    // index of -beta
 };
 
@@ -152,7 +154,7 @@ __device__ __forceinline__ void softmin_tile_f32(const float* __restrict__ rec,
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     S[2 * p] += f32_to_f64_alu(T[p].x);
-    S[2 * p + 1] += f32_to_f64_alu(T[p].y);
+    if (2 * p + 1 < R) S[2 * p + 1] += f32_to_f64_alu(T[p].y);
   }
 }
 
@@ -229,44 +231,60 @@ __global__ void __launch_bounds__(128, MINB) softmin_f32_kernel(const SoftminArg
 // ------------------------------------------------------------------------------
 // fp64 path
 // ------------------------------------------------------------------------------
-template <int KD, int SQ, int R, int G, int TILE>
-__device__ __forceinline__ void softmin_tile_f64(const double* __restrict__ rec,
-                                                 const double (&x)[R][KD], const double (&s)[R],
-                                                 double (&mq)[R], double (&S)[R]) {
+template <int KD, int SQ, int R, int G>
+__device__ __forceinline__ void f64_scores(const double* __restrict__ rec, const double (&x)[R][KD],
+                                           const double (&s)[R], double (&q)[R][G]) {
   using L = ColLayout<double, KD, SQ>;
-  float T[R];  // per-tile fp32 sums, folded into S once per tile (no per-group F2F)
 #pragma unroll
-  for (int r = 0; r < R; ++r) T[r] = 0.f;
-#pragma unroll 1
-  for (int j = 0; j < TILE; j += G) {
-    double q[R][G];
+  for (int g = 0; g < G; ++g) {
+    double c[L::kStride];
+    const double2* r2 = reinterpret_cast<const double2*>(rec + g * L::kStride);
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      double c[L::kStride];
-      const double2* r2 = reinterpret_cast<const double2*>(rec + (j + g) * L::kStride);
-#pragma unroll
-      for (int v = 0; v < L::kStride / 2; ++v) {
-        const double2 t = r2[v];
-        c[2 * v + 0] = t.x;
-        c[2 * v + 1] = t.y;
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        double acc = c[L::kBeta];
-#pragma unroll
-        for (int k = 0; k < KD; ++k) acc = fma(x[r][k], c[k], acc);
-        if (SQ) acc = fma(s[r], c[KD], acc);  // -2 lam s_i t_j; lam s_i^2 added per row
-        q[r][g] = acc;
-      }
+    for (int v = 0; v < L::kStride / 2; ++v) {
+      const double2 t = r2[v];
+      c[2 * v + 0] = t.x;
+      c[2 * v + 1] = t.y;
     }
-    // mq is the row reference carried kRefOffset above the smallest q seen, so
-    // terms are 2^(mq - q) in [0, 2^(16 + kRefOffset)] between rebases
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      float gsum = 0.f;
+      double acc = c[L::kBeta];
 #pragma unroll
-      for (int g = 0; g < G; ++g) gsum += ex2(f64_to_f32_fast(mq[r] - q[r][g]));
-      if (!(gsum <= kRebaseF64)) {  // rare: rebase at the group minimum
+      for (int k = 0; k < KD; ++k) acc = fma(x[r][k], c[k], acc);
+      if (SQ) acc = fma(s[r], c[KD], acc);  // -2 lam s_i t_j; lam s_i^2 added per row
+      q[r][g] = acc;
+    }
+  }
+}
+
+// Group sums 2^(mq - q) for row pairs (FADD2); an odd last row uses .x only.
+template <int R, int G>
+__device__ __forceinline__ void f64_group_sums(const double (&q)[R][G], const double (&mq)[R],
+                                               float2 (&gs)[(R + 1) / 2]) {
+#pragma unroll
+  for (int p = 0; p < (R + 1) / 2; ++p) {
+    const int r1 = 2 * p + 1 < R ? 2 * p + 1 : R - 1;
+    gs[p] = f2(0.f, 0.f);
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      gs[p] = add2(gs[p], f2(ex2(f64_to_f32_fast(mq[2 * p] - q[2 * p][g])),
+                             2 * p + 1 < R ? ex2(f64_to_f32_fast(mq[r1] - q[r1][g])) : 0.f));
+  }
+}
+
+// Rare path: a group sum left [0, kRebaseF64] (or is inf/NaN) -> rebase the
+// row reference kRefOffset above the group minimum and redo that row's sum.
+template <int R, int G>
+__device__ __forceinline__ void f64_fold(const double (&q)[R][G], double (&mq)[R], double (&S)[R],
+                                         float2 (&gs)[(R + 1) / 2], float2 (&T)[(R + 1) / 2]) {
+#pragma unroll
+  for (int p = 0; p < (R + 1) / 2; ++p) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = 2 * p + h;
+      if (r >= R) break;
+      float& gsum = h ? gs[p].y : gs[p].x;
+      float& tr = h ? T[p].y : T[p].x;
+      if (!(gsum <= kRebaseF64)) {
         double qmin = q[r][0];
 #pragma unroll
         for (int g = 1; g < G; ++g) qmin = fmin(qmin, q[r][g]);
@@ -274,18 +292,46 @@ __device__ __forceinline__ void softmin_tile_f64(const double* __restrict__ rec,
         if (ref < mq[r]) {
           const double sc = exp2(ref - mq[r]);
           S[r] *= sc;
-          T[r] *= (float)sc;
+          tr *= (float)sc;
           mq[r] = ref;
         }
         gsum = 0.f;
 #pragma unroll
         for (int g = 0; g < G; ++g) gsum += ex2(f64_to_f32_fast(mq[r] - q[r][g]));
       }
-      T[r] += gsum;
     }
+    T[p] = add2(T[p], gs[p]);
+  }
+}
+
+// One shared-memory tile of the fp64 path: per group of G columns, R x G
+// DFMA score chains, then the ALU conversion + MUFU.EX2 + FADD2 sums and the
+// (rare) rebase. Software-pipelining the next group's DFMA chains into the
+// current group's exponentials measured no faster: the per-pair mix (4 DFMA +
+// DADD + 3 ALU + EX2 + FADD) runs at the ceiling tools/ubench_f64mix measures
+// for it in isolation (~6.2 pairs/clk/SM).
+template <int KD, int SQ, int R, int G, int TILE>
+__device__ __forceinline__ void softmin_tile_f64(const double* __restrict__ rec,
+                                                 const double (&x)[R][KD], const double (&s)[R],
+                                                 double (&mq)[R], double (&S)[R]) {
+  using L = ColLayout<double, KD, SQ>;
+  constexpr int P = (R + 1) / 2;
+  float2 T[P];  // per-tile fp32 sums of row pairs, folded into S once per tile
+#pragma unroll
+  for (int p = 0; p < P; ++p) T[p] = f2(0.f, 0.f);
+#pragma unroll 1
+  for (int j = 0; j < TILE; j += G) {
+    double q[R][G];
+    float2 gs[P];
+    f64_scores<KD, SQ, R, G>(rec + j * L::kStride, x, s, q);
+    f64_group_sums<R, G>(q, mq, gs);
+    f64_fold<R, G>(q, mq, S, gs, T);
   }
 #pragma unroll
-  for (int r = 0; r < R; ++r) S[r] += f32_to_f64_alu(T[r]);
+  for (int p = 0; p < P; ++p) {
+    S[2 * p] += f32_to_f64_alu(T[p].x);
+    if (2 * p + 1 < R) S[2 * p + 1] += f32_to_f64_alu(T[p].y);
+  }
 }
 
 template <int KD, int SQ, int R, int G, int MINB, int TILE>

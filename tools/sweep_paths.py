@@ -63,9 +63,18 @@ def main(n=1 << 19, reps=3, rounds=3, only=None):
                           "CNTGW_L2_CHUNK_MB": str(l2)}))
     s4, t4, e4, p4 = build(n, 3, True)
     variants.append((f"C4-law K=3+sq prec={F32}", s4, t4, e4, p4, F32, {"CNTGW_L2_CHUNK_MB": "32"}))
-    for rg, l2 in (("0", 32), ("0", 0), ("44", 32), ("24", 32)):
-        variants.append((f"C4-law K=3+sq prec={F64} rg={rg} l2={l2}", s4, t4, e4, p4, F64,
-                         {"CNTGW_F64_RG": rg, "CNTGW_L2_CHUNK_MB": str(l2)}))
+    variants.append((f"C4-law K=3+sq prec={F64}", s4, t4, e4, p4, F64, {}))
+    # C5-shaped fp64 half-update (K=32 + sq), 2^18 x 2^18 scaled by (n/2^18)^2 in the print
+    n5 = min(n, 1 << 18)
+    rng = np.random.default_rng(5)
+    x5 = rng.standard_normal((n5, 32)) * 0.7
+    y5 = rng.standard_normal((n5, 32)) * 0.7
+    s5 = engine.Side.make(x5, 0.5 * (x5 * x5).sum(1), np.full(n5, 1 / n5), dev, 32)
+    t5 = engine.Side.make(y5, 0.5 * (y5 * y5).sum(1), np.full(n5, 1 / n5), dev, 32)
+    p5 = engine.to_dev64(rng.standard_normal(n5) * 10.0, dev)
+    for dm in ("1", "0"):
+        variants.append((f"C5-shape K=32+sq n={n5} prec={F64} dmma={dm}", s5, t5, 2.5e-3, p5, F64,
+                         {"CNTGW_F64_DMMA": dm}))
     if only:
         variants = [v for v in variants if all(tok in v[0] for tok in only.split(","))]
     results = {v[0]: [] for v in variants}
@@ -79,7 +88,8 @@ def main(n=1 << 19, reps=3, rounds=3, only=None):
             results[name] += time_variant(op, st, pot_, out, reps)
     for name, ms in results.items():
         med = statistics.median(ms)
-        print(f"{name:45s} {med:9.3f} ms  {n * n / (med * 1e-3):.3e} pairs/s", flush=True)
+        nn = int(name.split(" n=")[1].split()[0]) if " n=" in name else n
+        print(f"{name:45s} {med:9.3f} ms  {nn * nn / (med * 1e-3):.3e} pairs/s", flush=True)
 
 
 if __name__ == "__main__":
