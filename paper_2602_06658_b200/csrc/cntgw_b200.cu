@@ -110,12 +110,22 @@ KernelPick pick() {
     k.rows = rows_f64<KD>();
     k.smem = 2 * (size_t)T * ColLayout<double, KD, SQ>::kStride * sizeof(double);
     k.rec_bytes = ColLayout<double, KD, SQ>::kStride * sizeof(double);
-    if constexpr (KD >= 16) {  // wide features: the dot on the FP64 tensor pipe (DMMA)
-      if (env_int("CNTGW_F64_DMMA", 1)) {
-        constexpr int RG = KD >= 64 ? 2 : 4, TD = KD >= 64 ? 64 : 128;
-        k.fn = (void*)softmin_dmma_kernel<KD, SQ, RG, TD, 3>;
-        k.cta_rows = 32 * RG;
-        k.smem = 2 * (size_t)TD * ColLayout<double, KD, SQ>::kStride * sizeof(double);
+    // the dot on the FP64 tensor pipe (DMMA); CNTGW_F64_DMMA=0 keeps the DFMA kernel
+    if (env_int("CNTGW_F64_DMMA", 1)) {
+      // wide K: 4 row groups x 1 column tile per step (the A fragments dominate
+      // the registers); small K: 2 row groups x 4 column tiles per step (all 8
+      // MMAs of a step in flight before the epilogue). 2-stage column ring
+      // with per-warp release (StageRing; measured equal to a block barrier
+      // per tile, and to 4/6 stages).
+      constexpr int RG = KD >= 64 ? 2 : (KD >= 16 ? 4 : 2), NT = KD >= 16 ? 1 : 4;
+      constexpr int TD = KD >= 64 ? 64 : (KD >= 16 ? 128 : 256), MB = KD >= 16 ? 3 : 4;
+      k.fn = (void*)softmin_dmma_kernel<KD, SQ, RG, NT, TD, MB>;
+      k.cta_rows = 32 * RG;
+      k.smem = (size_t)2 * TD * ColLayout<double, KD, SQ>::kStride * sizeof(double);
+      if constexpr (KD < 16) {  // tuning alternatives (tools/sweep_paths.py)
+        const int v = env_int("CNTGW_DMMA_NT", 0);
+        if (v == 2) k.fn = (void*)softmin_dmma_kernel<KD, SQ, 4, 2, TD, MB>, k.cta_rows = 128;
+        if (v == 11) k.fn = (void*)softmin_dmma_kernel<KD, SQ, RG, NT, TD, MB, 2, 1>;
       }
     }
   }
@@ -304,7 +314,10 @@ int cntgw_col_stride(int prec, int kd, int sq) {
   if (!kd_supported(kd)) return fail(CNTGW_EINVAL, "unsupported feature width kd=%d", kd);
   const int raw = kd + (sq ? 1 : 0) + 1;
   if (prec == CNTGW_F32) return (raw + 3) / 4 * 4;
-  if (prec == CNTGW_F64) return kd >= 16 ? (raw + 3) / 4 * 4 : (raw + 1) / 2 * 2;
+  if (prec == CNTGW_F64) {
+    const int vec = (raw + 1) / 2 * 2, k4 = (kd + (sq ? 1 : 0) + 3) / 4 * 4;
+    return k4 > vec ? k4 : vec;
+  }
   if (prec == CNTGW_TF32X3) {
     if (sq || (kd != 8 && kd != 16))
       return fail(CNTGW_EINVAL, "tensor-core path supports kd in {8,16} without sq (kd=%d sq=%d)", kd, sq);

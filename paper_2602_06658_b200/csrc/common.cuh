@@ -155,6 +155,69 @@ struct TilePipe {
   }
 };
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// 2^x for two values on the FMA pipe (FA4-style MUFU offload): x clamped to
+// [-125, 64], split x = j + r with |r| <= 1/2 by the 1.5*2^23 rounding trick,
+// 2^r by a degree-5 minimax polynomial (max rel. error 2.3e-7 in fp32 Horner,
+// on par with MUFU.EX2), and j added to the exponent field with an integer op.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fminf(fmaxf(x.x, -125.f), 64.f);
+  x.y = fminf(fmaxf(x.y, -125.f), 64.f);
+  const float2 t = add2(x, f2(12582912.f, 12582912.f));
+  const float2 j = add2(t, f2(-12582912.f, -12582912.f));
+  const float2 r = fma2(j, f2(-1.f, -1.f), x);
+  float2 p = f2(1.3276470126584172e-3f, 1.3276470126584172e-3f);
+  p = fma2(p, r, f2(9.675541892647743e-3f, 9.675541892647743e-3f));
+  p = fma2(p, r, f2(5.550713464617729e-2f, 5.550713464617729e-2f));
+  p = fma2(p, r, f2(0.24022120237350464f, 0.24022120237350464f));
+  p = fma2(p, r, f2(0.6931469440460205f, 0.6931469440460205f));
+  p = fma2(p, r, f2(1.0000001192092896f, 1.0000001192092896f));
+  return f2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+            __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+
+// NS-stage ring of fixed-size column tiles with per-stage full (TMA bytes) and
+// empty (one arrival per warp) mbarriers: no block-wide barrier per tile.
+// Thread 0 is the producer; it refills the stage of tile t - LAG (with tile
+// t - LAG + NS) once every warp has released it, LAG = NS / 2 tiles behind its
+// own position, so it rarely waits.
+template <int NS>
+struct StageRing {
+  static constexpr int kLag = NS / 2 > 0 ? NS / 2 : 1;
+  uint64_t* full;
+  uint64_t* empty;
+  __device__ void init(int nwarps) {
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < NS; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], nwarps);
+      }
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
+  // thread 0 only: tile t into stage t % NS
+  __device__ void load(void* stage, const void* src, uint32_t bytes, int t) {
+    mbar_expect_tx(&full[t % NS], bytes);
+    bulk_g2s(stage, src, bytes, &full[t % NS]);
+  }
+  // thread 0 only, before consuming tile t: the tile to refill now, or -1
+  __device__ int refill_slot(int t, int ntiles) {
+    const int done = t - kLag;  // tile whose stage is recycled
+    if (done < 0 || done + NS >= ntiles) return -1;
+    mbar_wait(&empty[done % NS], (done / NS) & 1);
+    return done + NS;
+  }
+  __device__ void wait_full(int t) { mbar_wait(&full[t % NS], (t / NS) & 1); }
+  __device__ void release(int t) {  // every thread of the warp has finished tile t
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[t % NS]);
+  }
+};
+
 // skip modes: 1 = the loop is done; 2 = the loop ended on a symmetrized
 // threshold break (its tentatives are already the final ones)
 __device__ __forceinline__ bool skip_now(const cntgw_sweep_state* st, int skip) {

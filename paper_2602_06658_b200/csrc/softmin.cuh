@@ -54,9 +54,10 @@ template <typename T, int KD, int SQ>
 struct ColLayout {
   static constexpr int kRaw = KD + SQ + 1;
   static constexpr int kPerVec = 16 / sizeof(T);                        // elements per 16 B
-  // elements; fp64 records of wide features are padded to the DMMA k4 step
-  static constexpr int kStride = (sizeof(T) == 8 && KD >= 16) ? (kRaw + 3) / 4 * 4
-                                                              : (kRaw + kPerVec - 1) / kPerVec * kPerVec;
+  // elements; fp64 records also cover the DMMA k4 steps of [features | sq]
+  static constexpr int kVec = (kRaw + kPerVec - 1) / kPerVec * kPerVec;
+  static constexpr int kK4 = (KD + SQ + 3) / 4 * 4;
+  static constexpr int kStride = (sizeof(T) == 8 && kK4 > kVec) ? kK4 : kVec;
   static constexpr int kBeta = KD + SQ;                                    // index of -beta
 };
 

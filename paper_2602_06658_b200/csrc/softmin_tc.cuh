@@ -90,9 +90,6 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t* u = reinterpret_cast<uint32_t*>(v);
   asm volatile(
@@ -141,26 +138,6 @@ __global__ void prep_cols_tc_kernel(const cntgw_sweep_state* st, const float* fe
   } else {
     put(L::kHi + KD, -1.0e30f);  // padding column: 2^(t - max) == 0
   }
-}
-
-// 2^x for two values on the FMA pipe (FA4-style MUFU offload): x clamped to
-// [-125, 64], split x = j + r with |r| <= 1/2 by the 1.5*2^23 rounding trick,
-// 2^r by a degree-5 minimax polynomial (max rel. error 2.3e-7 in fp32 Horner,
-// on par with MUFU.EX2), and j added to the exponent field with an integer op.
-__device__ __forceinline__ float2 exp2_poly2(float2 x) {
-  x.x = fminf(fmaxf(x.x, -125.f), 64.f);
-  x.y = fminf(fmaxf(x.y, -125.f), 64.f);
-  const float2 t = add2(x, f2(12582912.f, 12582912.f));
-  const float2 j = add2(t, f2(-12582912.f, -12582912.f));
-  const float2 r = fma2(j, f2(-1.f, -1.f), x);
-  float2 p = f2(1.3276470126584172e-3f, 1.3276470126584172e-3f);
-  p = fma2(p, r, f2(9.675541892647743e-3f, 9.675541892647743e-3f));
-  p = fma2(p, r, f2(5.550713464617729e-2f, 5.550713464617729e-2f));
-  p = fma2(p, r, f2(0.24022120237350464f, 0.24022120237350464f));
-  p = fma2(p, r, f2(0.6931469440460205f, 0.6931469440460205f));
-  p = fma2(p, r, f2(1.0000001192092896f, 1.0000001192092896f));
-  return f2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
-            __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
 }
 
 // One 32-column chunk of the epilogue: terms 2^(v - mref) summed with FADD2

@@ -43,7 +43,8 @@ def test_abi_version_and_state_layout():
 
 @pytest.mark.parametrize("prec,kd,sq,stride", [
     (0, 1, 0, 4), (0, 3, 1, 8), (0, 4, 0, 8), (0, 16, 0, 20), (0, 32, 1, 36), (0, 64, 1, 68),
-    (1, 1, 0, 2), (1, 3, 1, 6), (1, 4, 0, 6), (1, 16, 0, 20), (1, 32, 1, 36), (1, 64, 1, 68)])
+    (1, 1, 0, 4), (1, 3, 1, 6), (1, 4, 0, 6), (1, 4, 1, 8), (1, 16, 0, 18), (1, 32, 1, 36),
+    (1, 64, 1, 68)])
 def test_column_record_stride(prec, kd, sq, stride):
     from paper_2602_06658_b200 import _native
 

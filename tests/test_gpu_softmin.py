@@ -97,6 +97,28 @@ def test_rebase_path_under_huge_exponents(env, prec):
     assert _rel(got, want) < (1e-5 if prec == 0 else 5e-7)
 
 
+@pytest.mark.parametrize("k", [1, 3, 4, 8, 16, 33, 64])
+def test_dmma_path_matches_dfma_path_cold(env, k, monkeypatch):
+    """fp64 half-update: the DMMA (m8n8k4 f64) kernel and the DFMA
+    kernel agree with the oracle and with each other in the cold regime
+    (exponents ~1e5 log2 units, lazy rebases), including ragged shapes."""
+    P, engine, S, O, torch, dev = env
+    rng = np.random.default_rng(k)
+    n, m = 531, 777
+    x = rng.standard_normal((n, k)) * 1.5
+    z = rng.standard_normal((m, k)) * 1.5
+    a, b = np.full(n, 1 / n), np.full(m, 1 / m)
+    g = rng.standard_normal(m) * 30.0 + (z * z).sum(1)
+    eps = 2.5e-3
+    want = O.softmin(O.SqEuclid(x, z), np.log(b), g, eps)
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("CNTGW_F64_DMMA", flag)
+        outs.append(_half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, 1))
+        assert _rel(outs[-1], want) < 5e-7, flag
+    assert _rel(outs[0], outs[1]) < 1e-9
+
+
 def test_deterministic_reruns(env):
     P, engine, S, O, torch, dev = env
     rng = np.random.default_rng(1)

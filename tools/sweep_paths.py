@@ -63,7 +63,9 @@ def main(n=1 << 19, reps=3, rounds=3, only=None):
                           "CNTGW_L2_CHUNK_MB": str(l2)}))
     s4, t4, e4, p4 = build(n, 3, True)
     variants.append((f"C4-law K=3+sq prec={F32}", s4, t4, e4, p4, F32, {"CNTGW_L2_CHUNK_MB": "32"}))
-    variants.append((f"C4-law K=3+sq prec={F64}", s4, t4, e4, p4, F64, {}))
+    for dm, nt in (("1", "0"), ("1", "2"), ("1", "11"), ("0", "0")):
+        variants.append((f"C4-law K=3+sq prec={F64} dmma={dm} nt={nt}", s4, t4, e4, p4, F64,
+                         {"CNTGW_F64_DMMA": dm, "CNTGW_DMMA_NT": nt}))
     # C5-shaped fp64 half-update (K=32 + sq), 2^18 x 2^18 scaled by (n/2^18)^2 in the print
     n5 = min(n, 1 << 18)
     rng = np.random.default_rng(5)
