@@ -150,6 +150,13 @@ def cpu_softmin_rate(inst, rows_target_s=10.0, threads=None, max_rows=4096):
     return rows * m / dt, dict(rows=rows, cols=m, seconds=dt, threads=threads)
 
 
+def workload_config(n, m, world):
+    """The `config` object of both arms (same workload, same keys)."""
+    return {"workload": "C2 softmin micro-benchmark (f-update + g-update per step)",
+            "n": n, "m": m, "k": C2["k"], "eps": C2["eps"], "parallelism": f"rows sharded x{world}",
+            "l2": "flushed by a 256 MiB write before every timed step"}
+
+
 def run_reference(args, info):
     """--impl reference: the CPU oracle on bounded samples of the same workload."""
     from paper_2602_06658_b200 import configs
@@ -172,11 +179,11 @@ def run_reference(args, info):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded C2 law)",
-        "config": {"workload": "C2 softmin micro-benchmark", "n": n, "m": n, "k": C2["k"],
-                   "eps": C2["eps"], "sample": "row samples at full M per step"},
+        "config": workload_config(n, n, args.gpus),
         "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port",
                          "sample": f"{sample['rows']} rows x {sample['cols']} cols f-update per step "
-                                   "(oracle/cntgw_oracle.py softmin, numpy+scipy logsumexp)"},
+                                   "(oracle/cntgw_oracle.py softmin, numpy+scipy logsumexp); "
+                                   "pairs/s of the sample stand for the full N x M step"},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -347,9 +354,7 @@ def run_b200(args, info):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded C2 law: u,v~N(0,1/16), a,b~U[0,1], g~N(0,1))",
-        "config": {"workload": "C2 softmin micro-benchmark (f-update + g-update per step)",
-                   "n": n, "m": m, "k": k, "eps": C2["eps"], "parallelism": f"rows sharded x{info.world}",
-                   "l2": "flushed by a 256 MiB write before every timed step"},
+        "config": workload_config(n, m, info.world),
         "roofline": {"bound": bound, "achieved": achieved, "peak": roof, "unit": "pairs/s",
                      "frac": achieved / roof, "traffic": traffic, "path": path, "model": model,
                      "peak_source": peaks["source"], "kernel_avg_ms": kern_avg_ms,

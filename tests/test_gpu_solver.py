@@ -178,3 +178,43 @@ def test_final_anneal_and_fixed_budget_graph(P):
     assert res.coupling.eps_eff > 0.01 / 8
     assert _rel(res.trace.objectives, ref["trace"]["objective"]) < TOL
     assert _rel(res.coupling.f, ref["f"]) < TOL
+
+
+def test_c3_eps_stage_chain_matches_reference(P):
+    """C3-law eps-stage loop (0.1 -> 0.00625, tau = 1e-5, warm potentials and
+    init='gamma' chained across stages) at N=400 against the reference's own
+    run: stage values, Gamma per stage, every inner-sweep count, and the
+    SolverError the reference raises at the 0.00625 stage."""
+    from dataclasses import replace
+
+    from paper_2602_06658_b200 import configs
+
+    gold = golden("c3law_stages")
+    src, tgt = _measures(P, gold)
+    prev, values, gammas, iters, lengths, err = None, [], [], [], [], ""
+    for eps in configs.C3_EPS_STAGES:
+        cfg = P.make_config(eps, threshold=1e-5, max_outer=10)
+        warm = None
+        if prev is not None:
+            cfg = replace(cfg, init="gamma", init_gamma=prev.gamma)
+            warm = (prev.coupling.f, prev.coupling.g)
+        try:
+            res = P.solve_cnt_gw(src, tgt, cfg, _warm_potentials=warm)
+        except P.SolverError as exc:
+            err = f"{eps}: {exc}"
+            break
+        prev = res
+        values.append(res.value)
+        gammas.append(res.gamma)
+        iters += list(res.trace.inner_iters)
+        lengths.append(len(res.trace))
+    assert err.split(":")[0] == str(gold["error"]).split(":")[0]
+    assert lengths == list(gold["stage_lengths"])
+    # the weighted-gap stop decision lands on the same sweep, or (when the gap
+    # crosses tau within rounding of the fp32 exponent path) one sweep apart
+    diff = np.abs(np.array(iters) - gold["inner_iters"])
+    assert diff.max() <= 1 and (diff > 0).sum() <= 2, list(diff)
+    assert _rel(values, gold["values"]) < TOL
+    assert _rel(np.array(gammas), gold["gammas"]) < TOL
+    assert _rel(prev.coupling.f, gold["f"]) < TOL
+    assert _rel(prev.coupling.g, gold["g"]) < TOL
