@@ -268,6 +268,46 @@ def cnt_reductions(f, g, cost, x, a, y, b, eps):
     return pi_y, sig, klv, rerr + float(np.abs(col - b).sum())
 
 
+def plan_reductions(f, g, cost, a, b, eps, x, y):
+    """(pi Y, pi s_y, pi^T X, pi^T s_x, sigma_ss) in one blocked pass
+    (divergence.py:72-86)."""
+    sx = 0.5 * np.einsum("ij,ij->i", x, x)
+    sy = 0.5 * np.einsum("ij,ij->i", y, y)
+    pi_y = np.empty((x.shape[0], y.shape[1]))
+    pi_sy = np.empty(x.shape[0])
+    pit_x = np.zeros((y.shape[0], x.shape[1]))
+    pit_sx = np.zeros(y.shape[0])
+    for i0, i1, p in plan_blocks(f, g, cost, a, b, eps):
+        pi_y[i0:i1] = p @ y
+        pi_sy[i0:i1] = p @ sy
+        pit_x += p.T @ x[i0:i1]
+        pit_sx += p.T @ sx[i0:i1]
+    return pi_y, pi_sy, pit_x, pit_sx, float(sx @ pi_sy)
+
+
+def grad_constant(x, a, other_trace):
+    """Per-point gradient of Q - 4 T T_other, O(N^2 D) blocks (divergence.py:138-150)."""
+    sq_norms = (x**2).sum(axis=1)
+    out = np.empty_like(x)
+    for i0 in range(0, x.shape[0], BLOCK):
+        i1 = min(i0 + BLOCK, x.shape[0])
+        diff = x[i0:i1, None, :] - x[None, :, :]
+        sq = np.maximum(sq_norms[i0:i1, None] + sq_norms[None, :] - 2.0 * (x[i0:i1] @ x.T), 0.0)
+        out[i0:i1] = 8.0 * a[i0:i1, None] * np.einsum("mk,mkd->md", sq * a[None, :], diff)
+    out -= 8.0 * other_trace * a[:, None] * x
+    return out
+
+
+def feature_gradients(x, a, y, b, gamma, red):
+    """Envelope gradients from the plan reductions (divergence.py:153-172)."""
+    pi_y, pi_sy, pit_x, pit_sx, _ = red
+    tx = float(a @ (x**2).sum(1))
+    ty = float(b @ (y**2).sum(1))
+    gsrc = grad_constant(x, a, ty) - 16.0 * (pi_y @ gamma.T + x * pi_sy[:, None])
+    gtgt = grad_constant(y, b, tx) - 16.0 * (pit_x @ gamma + y * pit_sx[:, None])
+    return gsrc, gtgt
+
+
 def solve_cnt_gw(x, a, y, b, eps, inner, max_outer=200, delta_outer=1e-5,
                  gamma0=None, warm=None, final_anneal=None):
     """Feature-space EGW alternate minimisation (solvers.py:285-350, 556-632).

@@ -648,34 +648,41 @@ def pi_step(gamma, src, tgt, eps: float, inner: SinkhornConfig):
     return sinkhorn(src.weights, tgt.weights, cost, inner.with_temperature(eps / 8.0))
 
 
-def _plan_pass(coupling, src, tgt):
+def _plan_pass(coupling, src, tgt, transpose: bool = False):
     """Fused K4 pass over an ImplicitCoupling on a SquaredEuclideanCost
-    (augmented features): returns device (r, pi Y, pi s, argmax)."""
+    (augmented features): returns device (r, pi Y, pi s_y, argmax) — or, with
+    ``transpose``, the same pass over pi^T: (c, pi^T X, pi^T s_x, argmax_i),
+    the column-side reductions of divergence._plan_reductions."""
     cost = coupling.cost
     if not isinstance(cost, SquaredEuclideanCost):
         raise TypeError("fused plan reductions need a SquaredEuclideanCost coupling")
     dev = engine.require_cuda()
     x, z = cost._x, cost._z
+    f_ref, g_ref = coupling.f, coupling.g
+    a_w, b_w = coupling.source_weights, coupling.target_weights
+    acc, acc_s = np.asarray(tgt.features), _half_sq(tgt)
+    if transpose:
+        x, z, f_ref, g_ref, a_w, b_w = z, x, g_ref, f_ref, b_w, a_w
+        acc, acc_s = np.asarray(src.features), _half_sq(src)
     xf, zf = x[:, :-1], z[:, :-1]
     kd = engine.padded_kd(max(1, xf.shape[1]))
-    e = np.asarray(tgt.features).shape[1]
+    e = acc.shape[1]
     from .sinkhorn import feature_problem
 
-    srcs, _, fwd, _ = feature_problem(xf, x[:, -1], zf, z[:, -1], coupling.source_weights,
-                                      coupling.target_weights, dev)
-    f = engine.to_dev64(coupling.f - (xf * xf).sum(1), dev)
-    g = engine.to_dev64(coupling.g - (zf * zf).sum(1), dev)
+    srcs, _, fwd, _ = feature_problem(xf, x[:, -1], zf, z[:, -1], a_w, b_w, dev)
+    f = engine.to_dev64(f_ref - (xf * xf).sum(1), dev)
+    g = engine.to_dev64(g_ref - (zf * zf).sum(1), dev)
     st = engine.SweepState(dev)
     st.init(coupling.eps_eff)
     fwd.pack(st, g, prec=F64)
-    n, m = cost.shape
+    n, m = x.shape[0], z.shape[0]
     r = torch.empty(n, dtype=torch.float64, device=dev)
     pi_y = torch.empty(n * e, dtype=torch.float64, device=dev)
     pi_s = torch.empty(n, dtype=torch.float64, device=dev)
     am = torch.empty(n, dtype=torch.int64, device=dev)
     ws = torch.empty(int(LIB.cntgw_plan_reduce_workspace(n, m, kd, e)), dtype=torch.uint8, device=dev)
-    y = engine.to_dev64(tgt.features, dev)
-    ty = engine.to_dev64(_half_sq(tgt), dev)
+    y = engine.to_dev64(acc, dev)
+    ty = engine.to_dev64(acc_s, dev)
     call("cntgw_plan_reduce", st.ptr, kd, e, srcs.feat64.data_ptr(), kd, srcs.sq64.data_ptr(),
          f.data_ptr(), srcs.log2w.data_ptr(), fwd.rec.data_ptr(), y.data_ptr(), e, ty.data_ptr(),
          n, m, r.data_ptr(), pi_y.data_ptr(), pi_s.data_ptr(), am.data_ptr(), ws.data_ptr(),

@@ -277,6 +277,42 @@ def gen_sinkhorn_cases():
     return out
 
 
+def gen_gradients():
+    """Plan reductions, loss decomposition, envelope gradients, SGW and a short
+    gradient flow (reference divergence.py:72-410) on C1-law clouds."""
+    from cntgw import divergence as dv
+
+    pc = configs.c1(seed=3, n=300, m=240)
+    src = _embed(pc.x, pc.a, 3)
+    tgt = _embed(pc.y, pc.b, 3)
+    cfg = cntgw.make_config(0.05, n_inner=60, max_outer=6, delta_outer=1e-12)
+    res = cntgw.solve_cnt_gw(src, tgt, cfg)
+    pi_y, pi_sy, pit_x, pit_sx, sigma_ss = dv._plan_reductions(res.coupling, src, tgt)
+    gsrc, gtgt = dv.feature_gradients(src, tgt, res.gamma, res.coupling)
+    rep = dv.gw_value_report(res.gamma, res.coupling, src, tgt, 0.05)
+    ql = dv.quartic_loss(res.coupling, src, tgt)
+    gc = dv._grad_constant(src, tgt.trace_second_moment())
+    sg = dv.sgw(src, tgt, cfg)
+    rng = np.random.default_rng(11)
+    pts = (rng.standard_normal((40, 3)) * 0.5).astype(np.float32).astype(np.float64)
+    tpts = (rng.standard_normal((50, 3)) * 0.6).astype(np.float32).astype(np.float64)
+    tau = _embed(tpts, np.full(50, 1.0 / 50), 3)
+    fcfg = cntgw.make_config(0.1, n_inner=40, max_outer=4, delta_outer=1e-12)
+    fl = dv.gradient_flow(cntgw.DiscreteMeasure(pts, np.full(40, 1.0 / 40)), [(1.0, tau)], fcfg,
+                          steps=3, step_size=0.05)
+    return dict(x_feat=src.features, y_feat=tgt.features, a=src.weights, b=tgt.weights,
+                gamma=res.gamma, value=res.value, f=res.coupling.f, g=res.coupling.g,
+                zbar=res.coupling.cost._z, eps_eff=res.coupling.eps_eff,
+                pi_y=pi_y, pi_sy=pi_sy, pit_x=pit_x, pit_sx=pit_sx, sigma_ss=sigma_ss,
+                gsrc=gsrc, gtgt=gtgt, grad_const=gc, quartic=ql,
+                report=np.array([rep.value, rep.constant, rep.gamma_sq, rep.kl_term,
+                                 rep.cross_term, rep.sigma_ss]),
+                sgw_value=sg.value, sgw_parts=np.array([sg.cross.value, sg.self_src.value,
+                                                        sg.self_tgt.value]),
+                flow_points=pts, flow_tau=tpts, flow_positions=np.array(fl.positions),
+                flow_objectives=np.array(fl.objectives))
+
+
 GENS = {
     "c1_solve": gen_c1,
     "c4law_solve": lambda: gen_law("C4", 1024, configs.C4_EPS, dict(n_inner=100), 10),
@@ -285,6 +321,7 @@ GENS = {
     "c2_subsample": gen_c2_subsample,
     "c2_small": gen_c2_small,
     "sinkhorn_cases": gen_sinkhorn_cases,
+    "gradients": gen_gradients,
 }
 
 

@@ -128,3 +128,20 @@ class TestKnownAnswers:
 
     def test_weighted_gap_cap(self):
         assert np.isfinite(O.weighted_gap(np.ones(2), np.array([1e6, 0]), np.zeros(2), 1e-3))
+
+
+def test_oracle_plan_reductions_and_gradients():
+    """Oracle restatement of divergence._plan_reductions / _grad_constant /
+    feature_gradients against the reference's own outputs (golden 'gradients')."""
+    gold = golden("gradients")
+    x, y, a, b = gold["x_feat"], gold["y_feat"], gold["a"], gold["b"]
+    cost = O.SqEuclid(O.augment(x), gold["zbar"])
+    red = O.plan_reductions(gold["f"], gold["g"], cost, a, b, float(gold["eps_eff"]), x, y)
+    for got, key in zip(red[:4], ("pi_y", "pi_sy", "pit_x", "pit_sx")):
+        assert _rel(got, gold[key]) < 1e-10, key
+    assert red[4] == pytest.approx(float(gold["sigma_ss"]), rel=1e-10)
+    ty = float(b @ (y**2).sum(1))
+    assert _rel(O.grad_constant(x, a, ty), gold["grad_const"]) < 1e-10
+    gsrc, gtgt = O.feature_gradients(x, a, y, b, gold["gamma"], red)
+    assert _rel(gsrc, gold["gsrc"]) < 1e-10
+    assert _rel(gtgt, gold["gtgt"]) < 1e-10
