@@ -230,6 +230,30 @@ int cntgw_graph_end(void* stream, void** exec_out);
 int cntgw_graph_launch(void* exec, void* stream);
 int cntgw_graph_destroy(void* exec);
 
+/* ---- multiscale front end: weighted k-means (solvers.py:668-726) -------
+ * Bit-compatible with the reference's numpy _weighted_kmeans (pairwise
+ * distance sums, first argmin, Generator.choice draws, index-order centre
+ * sums). Points x: n x d fp64 contiguous, d in {1..8, 16, 32, 64}.
+ * k-means++ draw j: p = w (d2 == NULL) or w*d2 / pairwise_sum(w*d2) (w if the
+ * sum is 0); idx = first i with cumsum(p)_i / cumsum(p)_{n-1} > u[j] (device
+ * u). leaf_off: nleaves+1 offsets of numpy's pairwise-sum leaves of n. */
+size_t cntgw_km_draw_workspace(int64_t n, int nleaves);
+int cntgw_km_draw(const double* w, const double* d2, int64_t n, const int64_t* leaf_off,
+                  int nleaves, const double* u, int j, int64_t* out_idx, void* workspace,
+                  size_t workspace_bytes, void* stream);
+/* center_out = x[*idx]; d2 = |x - center|^2 (first) or min(d2, |x - center|^2) */
+int cntgw_km_update_d2(const double* x, int64_t n, int d, const int64_t* idx, double* center_out,
+                       double* d2, int first, void* stream);
+/* assign_i = first argmin_j |x_i - c_j|^2, own_i = that distance */
+int cntgw_km_assign(const double* x, int64_t n, int d, const double* centers, int64_t k,
+                    int64_t* assign, double* own, void* stream);
+/* per listed cluster c (id ids[c], or c): members[offsets[c]:offsets[c+1]] in
+ * index order -> centers[id] = sum fl(w x) / pairwise_sum(w) (skipped when
+ * empty), or, if masses != NULL, masses[id] = sequential sum of w. */
+int cntgw_km_centers(const double* x, int d, const double* w, const int64_t* members,
+                     const int64_t* offsets, int64_t ncl, const int64_t* ids, double* centers,
+                     double* masses, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -721,3 +721,7 @@ def egw_objective(gamma, coupling, src, tgt, eps: float) -> float:
     cross = float((gamma * xt_pi_y).sum()) + sigma_ss
     const = divergence.constant_value(src, tgt)
     return const + 8.0 * (float((gamma**2).sum()) + (eps / 8.0) * kl - 2.0 * cross)
+
+
+# multiscale front end (reference solvers.py:668-763), device k-means
+from .multiscale import _weighted_kmeans, coarsen, solve_multiscale  # noqa: E402,F401

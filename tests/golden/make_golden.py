@@ -313,6 +313,40 @@ def gen_gradients():
                 flow_objectives=np.array(fl.objectives))
 
 
+def gen_multiscale():
+    """Weighted k-means (incl. empty clusters and D=64), coarsen and the
+    two-stage solve (reference solvers.py:668-763)."""
+    from cntgw import solvers as rs
+
+    out = {}
+    rng = np.random.default_rng(21)
+    cases = {}
+    pc = configs.c1(seed=5, n=1000)
+    cases["c1"] = (np.ascontiguousarray(pc.x - pc.x.mean(0)), np.full(1000, 1e-3), 100)
+    xw = (rng.standard_normal((600, 3)) * [1.0, 0.5, 2.0]).astype(np.float32).astype(np.float64)
+    ww = rng.dirichlet(np.ones(600))
+    cases["dirichlet"] = (xw, ww, 37)
+    base = (rng.standard_normal((3, 2))).astype(np.float32).astype(np.float64)
+    xd = base[rng.integers(0, 3, 24)]
+    cases["dupes"] = (xd, np.full(24, 1.0 / 24), 6)
+    x64 = (rng.standard_normal((300, 64)) * 0.7).astype(np.float32).astype(np.float64)
+    cases["d64"] = (x64, np.full(300, 1.0 / 300), 20)
+    for name, (x, w, k) in cases.items():
+        assign, centers, cw = rs._weighted_kmeans(x, w, k, np.random.default_rng(7))
+        out.update({f"{name}__x": x, f"{name}__w": w, f"{name}__k": np.array(k),
+                    f"{name}__assign": assign, f"{name}__centers": centers, f"{name}__cw": cw})
+    pc = configs.c1(seed=0)
+    src = _embed(pc.x, pc.a, 3)
+    tgt = _embed(pc.y, pc.b, 3)
+    cfg = cntgw.make_config(configs.C1_EPS, threshold=1e-5, max_inner=200, max_outer=20)
+    res = rs.solve_multiscale(src, tgt, cfg, rho=0.1)
+    out.update(ms_x=src.features, ms_y=tgt.features, ms_a=src.weights, ms_b=tgt.weights,
+               ms_value=res.value, ms_gamma=res.gamma, ms_f=res.coupling.f, ms_g=res.coupling.g,
+               ms_inner=np.array(res.trace.inner_iters), ms_coarse_value=res.coarse.value,
+               ms_coarse_gamma=res.coarse.gamma, ms_coarse_inner=np.array(res.coarse.trace.inner_iters))
+    return out
+
+
 GENS = {
     "c1_solve": gen_c1,
     "c4law_solve": lambda: gen_law("C4", 1024, configs.C4_EPS, dict(n_inner=100), 10),
@@ -322,6 +356,7 @@ GENS = {
     "c2_small": gen_c2_small,
     "sinkhorn_cases": gen_sinkhorn_cases,
     "gradients": gen_gradients,
+    "multiscale": gen_multiscale,
 }
 
 

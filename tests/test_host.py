@@ -179,3 +179,18 @@ class TestGenerators:
         inst = configs.c2(seed=0, n=4096, k=16)
         assert inst.u.shape == (4096, 16) and inst.u.dtype == np.float32
         assert inst.u.std() == pytest.approx(0.25, rel=0.05)
+
+
+def test_coarsen_validation():
+    """coarsen rejects rho outside (0, 1) and fewer than 2 clusters before
+    touching the device (reference solvers.py:714-721)."""
+    import pytest as _pt
+
+    from paper_2602_06658_b200 import EmbeddedMeasure, coarsen
+
+    m = EmbeddedMeasure(np.zeros((10, 2)), np.full(10, 0.1))
+    rng = np.random.default_rng(0)
+    with _pt.raises(ValueError, match="rho must lie"):
+        coarsen(m, 1.0, rng)
+    with _pt.raises(ValueError, match="need at least 2"):
+        coarsen(m, 0.05, rng)
