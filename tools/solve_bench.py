@@ -4,6 +4,7 @@
     python tools/solve_bench.py c4 [n] [outer] # C4 law, fixed 100-sweep inner budget
     python tools/solve_bench.py c5 [n] [outer] # C5 law, fixed 200-sweep inner budget
     python tools/solve_bench.py c3 [n]         # C3 eps-stage loop (tau = 1e-5)
+    python tools/solve_bench.py ms [n]         # multiscale vs direct, C1 law
 
 C4/C5 time the fixed number of outer steps the config names, stepping the
 solver state without the stop rule (the cold laws trip the reference's own
@@ -95,6 +96,34 @@ def main():
         torch.cuda.synchronize()
         out = dict(config="C3", n=n, seconds=time.perf_counter() - t0, stage_values=values,
                    error=err)
+    elif which == "ms":
+        # multiscale front end on the C1 law at larger N: k-means coarsening
+        # (rho = 0.1) + coarse + fine solve, against the direct solve
+        from paper_2602_06658_b200 import multiscale
+
+        n = args[0] if args else 100_000
+        pc = configs.c1(seed=0, n=n)
+        src, tgt = measures(pc)
+        cfg = P.make_config(configs.C1_EPS, threshold=1e-5, max_inner=200, max_outer=20)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rng = np.random.default_rng(cfg.seed)
+        multiscale.coarsen(src, 0.1, rng)
+        torch.cuda.synchronize()
+        t_km = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        res = P.solve_multiscale(src, tgt, cfg, rho=0.1)
+        torch.cuda.synchronize()
+        t_ms = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        direct = P.solve_cnt_gw(src, tgt, cfg)
+        torch.cuda.synchronize()
+        t_dir = time.perf_counter() - t0
+        out = dict(config="C1-law multiscale", n=n, k=int(np.ceil(0.1 * n)),
+                   kmeans_one_side_s=t_km, multiscale_s=t_ms, direct_s=t_dir,
+                   multiscale_value=res.value, direct_value=direct.value,
+                   fine_inner=res.trace.inner_iters, coarse_inner=res.coarse.trace.inner_iters,
+                   direct_inner=direct.trace.inner_iters)
     else:
         raise SystemExit(f"unknown config {which}")
     print(json.dumps(out), flush=True)
