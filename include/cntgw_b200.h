@@ -230,6 +230,19 @@ int cntgw_graph_end(void* stream, void** exec_out);
 int cntgw_graph_launch(void* exec, void* stream);
 int cntgw_graph_destroy(void* exec);
 
+/* ---- kernel PCA: matrix-free cost products (kernels.py:149-345) --------
+ * out (n x bcols) = C V with C_ij = c(x_i, x_j) evaluated on the fly in fp64
+ * from sq = |x_i|^2 + |x_j|^2 - 2 x_i.x_j clipped at 0 (sqn = |x|^2), c_ii = 0;
+ * V: n x bcols row-major, bcols in {8, 16, 32, 64}; par = p (p_norm) or sigma. */
+enum cntgw_cost_kind {
+  CNTGW_COST_SQEUCLID = 0,
+  CNTGW_COST_EUCLIDEAN = 1,
+  CNTGW_COST_PNORM = 2,
+  CNTGW_COST_EXP = 3
+};
+int cntgw_cost_product(int kind, double par, const double* x, int64_t n, int d, const double* sqn,
+                       const double* v, int bcols, double* out, void* stream);
+
 /* ---- multiscale front end: weighted k-means (solvers.py:668-726) -------
  * Bit-compatible with the reference's numpy _weighted_kmeans (pairwise
  * distance sums, first argmin, Generator.choice draws, index-order centre

@@ -347,6 +347,53 @@ def gen_multiscale():
     return out
 
 
+def gen_kpca():
+    """Kernel-PCA embeddings for every cost kind (dense branch, N=300), the
+    subspace branch (N=4500 > 4096), centred kernels, the CNT diagnostic, cost
+    matrices and gradients (reference kernels.py:149-446)."""
+    from cntgw import kernels as rk
+
+    rng = np.random.default_rng(8)
+    pts = (rng.standard_normal((300, 5)) * [1.0, 0.8, 0.6, 0.4, 0.2]).astype(np.float32).astype(np.float64)
+    w = rng.dirichlet(np.ones(300))
+    emb6 = (rng.standard_normal((300, 6))).astype(np.float32).astype(np.float64)
+    meas = cntgw.DiscreteMeasure(pts, w)
+    dense_c = rk.cost_matrix(rk.CostSpec("euclidean"), meas)
+    specs = {
+        "euclid": (rk.CostSpec("euclidean"), 4),
+        "pnorm": (rk.CostSpec("p_norm", p=1.5), 4),
+        "exp": (rk.CostSpec("exp_kernel", sigma=0.8), 4),
+        "sqlow": (rk.CostSpec("sq_euclidean"), 2),
+        "embed": (rk.CostSpec("precomputed_embedding", path="mem", payload=emb6), 3),
+        "matrix": (rk.CostSpec("dense_matrix", path="mem", payload=dense_c), 4),
+    }
+    out = dict(pts=pts, w=w, emb6=emb6)  # the dense_matrix payload is the euclidean cost of pts
+    for name, (spec, dim) in specs.items():
+        e = rk.embed_measure(meas, spec, dim=dim)
+        out.update({f"{name}__f": e.features, f"{name}__ev": np.array(e.explained_variance),
+                    f"{name}__vals": e.eigenvalues, f"{name}__dim": np.array(dim)})
+    big = (rng.standard_normal((4500, 3)) * [1.0, 0.7, 0.4]).astype(np.float32).astype(np.float64)
+    wb = np.full(4500, 1.0 / 4500)
+    eb = rk.embed_measure(cntgw.DiscreteMeasure(big, wb), rk.CostSpec("euclidean"), dim=3)
+    out.update(big=big, big__f=eb.features, big__vals=eb.eigenvalues, big__ev=np.array(eb.explained_variance))
+    small = pts[:40]
+    ws = np.full(40, 1.0 / 40)
+    c40 = rk.cost_matrix(rk.CostSpec("euclidean"), cntgw.DiscreteMeasure(small, ws))
+    kern = rk.kernel_from_cost(c40, ws, base_index=3)
+    diag = rk.cnt_diagnostic(c40, ws)
+    rnd = rng.random((40, 40))
+    rnd = rnd + rnd.T
+    np.fill_diagonal(rnd, 0.0)
+    diag2 = rk.cnt_diagnostic(rnd, ws)
+    out.update(c40=c40, k40=kern.matrix, diag=np.array([diag.min_eigenvalue, diag.max_abs_eigenvalue,
+                                                         float(diag.is_cnt)]),
+               rnd=rnd, diag2=np.array([diag2.min_eigenvalue, diag2.max_abs_eigenvalue, float(diag2.is_cnt)]),
+               cexp=rk.cost_matrix(rk.CostSpec("exp_kernel", sigma=0.8), cntgw.DiscreteMeasure(small, ws)),
+               gexp=rk.cost_gradients(rk.CostSpec("exp_kernel", sigma=0.8), small[:20]),
+               gpn=rk.cost_gradients(rk.CostSpec("p_norm", p=1.5), small[:20]))
+    return out
+
+
 GENS = {
     "c1_solve": gen_c1,
     "c4law_solve": lambda: gen_law("C4", 1024, configs.C4_EPS, dict(n_inner=100), 10),
@@ -357,6 +404,7 @@ GENS = {
     "sinkhorn_cases": gen_sinkhorn_cases,
     "gradients": gen_gradients,
     "multiscale": gen_multiscale,
+    "kpca": gen_kpca,
 }
 
 

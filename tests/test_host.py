@@ -138,10 +138,42 @@ class TestEmbedding:
         assert np.allclose(emb.augmented()[:, -1], emb.half_sq_norms)
         assert emb.trace_second_moment() == pytest.approx(float(np.trace(emb.covariance())))
 
-    def test_kernel_pca_is_out_of_scope(self):
+    def test_kernel_pca_runs_on_the_device_only(self):
+        """Kernel-PCA embeddings have no CPU fallback (the CPU suite has no GPU)."""
         m = P.DiscreteMeasure(np.random.default_rng(0).standard_normal((10, 5)))
-        with pytest.raises(NotImplementedError):
+        with pytest.raises(RuntimeError, match="CUDA device"):
             P.embed_measure(m, P.CostSpec("sq_euclidean"), dim=2)
+        with pytest.raises(ValueError, match="exceeds support size"):
+            P.embed_measure(m, P.CostSpec("euclidean"), dim=11)
+
+    def test_cost_spec_grammar_and_validation(self):
+        from paper_2602_06658_b200 import kernels as K
+
+        assert K.parse_cost_spec("p_norm:1.5").p == 1.5
+        assert K.parse_cost_spec("exp:0.3").sigma == 0.3
+        assert K.parse_cost_spec(" euclidean ").kind == "euclidean"
+        assert K.CostSpec("p_norm", p=1.5).differentiable and not K.CostSpec("euclidean").differentiable
+        assert K.CostSpec("exp_kernel", sigma=2.0).describe() == "exp:2"
+        for bad in ("p_norm:x", "exp:", "cosine", "foo:1"):
+            with pytest.raises(ValueError):
+                K.parse_cost_spec(bad)
+        with pytest.raises(ValueError, match="exponent"):
+            K.CostSpec("p_norm", p=2.5)
+        with pytest.raises(ValueError, match="radius"):
+            K.CostSpec("exp_kernel", sigma=0.0)
+        with pytest.raises(ValueError, match="payload"):
+            K.CostSpec("dense_matrix")
+
+    def test_matrix_payload_checks(self, tmp_path):
+        from paper_2602_06658_b200 import kernels as K
+
+        good = tmp_path / "c.csv"
+        good.write_text("0,1,2\n1,0,1\n2,1,0\n")
+        assert K.parse_cost_spec(f"matrix:{good}").payload.shape == (3, 3)
+        bad = tmp_path / "b.csv"
+        bad.write_text("0,1\n2,0\n")
+        with pytest.raises(ValueError, match="symmetric"):
+            K.load_matrix_payload(bad)
 
 
 def test_solve_trace_csv(tmp_path):
