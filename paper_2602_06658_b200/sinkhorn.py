@@ -40,25 +40,42 @@ class DenseCost:
     """Explicit cost matrix (reference sinkhorn.py:30-56)."""
 
     def __init__(self, matrix):
+        self._dev = None
+        if isinstance(matrix, torch.Tensor):  # device-resident (dense GW baselines)
+            if matrix.ndim != 2:
+                raise ValueError("cost matrix must be 2-dimensional")
+            if not bool(torch.isfinite(matrix).all()):
+                raise ValueError("cost matrix contains non-finite entries")
+            self._dev = matrix.to(torch.float64).contiguous()
+            self._m = None
+            self._shape = tuple(self._dev.shape)
+            self._t = None
+            return
         m = np.ascontiguousarray(matrix, dtype=np.float64)
         if m.ndim != 2:
             raise ValueError("cost matrix must be 2-dimensional")
         if not np.isfinite(m).all():
             raise ValueError("cost matrix contains non-finite entries")
         self._m = m
+        self._shape = m.shape
         self._t = None
 
-    shape = property(lambda self: self._m.shape)
+    shape = property(lambda self: self._shape)
+
+    def _host(self):
+        if self._m is None:
+            self._m = self._dev.cpu().numpy()
+        return self._m
 
     def rows(self, i0, i1):
-        return self._m[i0:i1]
+        return self._host()[i0:i1]
 
     def full(self):
-        return self._m
+        return self._host()
 
     def transpose(self) -> "DenseCost":
         if self._t is None:
-            self._t = DenseCost(self._m.T)
+            self._t = DenseCost(self._dev.t() if self._dev is not None else self._m.T)
             self._t._t = self
         return self._t
 
@@ -249,8 +266,11 @@ def device_problem(cost, a, b, device) -> DeviceProblem:
             f"cost provider {type(cost).__name__} has no feature form and {n}x{m} entries is too "
             "large to stream densely; use SquaredEuclideanCost or SeparableLowRankCost"
         )
-    dense = cost.full() if hasattr(cost, "full") else cost.rows(0, n)
-    c = torch.as_tensor(np.ascontiguousarray(dense), dtype=torch.float32, device=device)
+    if getattr(cost, "_dev", None) is not None:
+        c = cost._dev.to(device=device, dtype=torch.float32).contiguous()
+    else:
+        dense = cost.full() if hasattr(cost, "full") else cost.rows(0, n)
+        c = torch.as_tensor(np.ascontiguousarray(dense), dtype=torch.float32, device=device)
     la = torch.log2(engine.to_dev64(a, device))
     lb = torch.log2(engine.to_dev64(b, device))
     fwd = engine.DenseHalfUpdate(c, lb)

@@ -628,11 +628,17 @@ def solve_cnt_gw(src, tgt, cfg: EgwConfig, _warm_potentials=None) -> EgwResult:
 
 
 def solve_adaptive(solver, *args, cfg: EgwConfig) -> EgwResult:
-    """Inner-budget doubling wrapper (reference solvers.py:652-665); the GPU
-    build serves the feature-space solver only."""
-    if solver is not solve_cnt_gw:
-        raise ValueError("solver must be solve_cnt_gw (dense solver families are out of scope)")
-    return _run_outer(_CntGwState(*args, cfg), cfg, adaptive=True)
+    """Inner-budget doubling wrapper (reference solvers.py:652-665) around
+    solve_cnt_gw, solve_kernel_gw or solve_entropic_gw."""
+    from .dense_solvers import _EntropicGwState, _KernelGwState, solve_entropic_gw, solve_kernel_gw
+
+    states = {solve_cnt_gw: _CntGwState, solve_kernel_gw: _KernelGwState,
+              solve_entropic_gw: _EntropicGwState}
+    try:
+        state_cls = states[solver]
+    except (TypeError, KeyError):
+        raise ValueError("solver must be one of the solve_* functions of this module") from None
+    return _run_outer(state_cls(*args, cfg), cfg, adaptive=True)
 
 
 # ---------------------------------------------------------------------------
@@ -725,3 +731,5 @@ def egw_objective(gamma, coupling, src, tgt, eps: float) -> float:
 
 # multiscale front end (reference solvers.py:668-763), device k-means
 from .multiscale import _weighted_kmeans, coarsen, solve_multiscale  # noqa: E402,F401
+# dense-plan baselines (reference solvers.py:384-553, 629-638)
+from .dense_solvers import solve_entropic_gw, solve_kernel_gw  # noqa: E402,F401

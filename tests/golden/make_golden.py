@@ -394,6 +394,31 @@ def gen_kpca():
     return out
 
 
+def gen_dense():
+    """Dense-plan baselines: kernel-trick EGW and classical Entropic-GW, plus the
+    adaptive wrapper around the kernel solver (reference solvers.py:384-665)."""
+    from cntgw import kernels as rk
+    from cntgw import solvers as rs
+
+    pc = configs.c1(seed=9, n=120, m=100)
+    mx = cntgw.DiscreteMeasure(pc.x, pc.a)
+    my = cntgw.DiscreteMeasure(pc.y, pc.b)
+    cx = rk.cost_matrix(rk.CostSpec("sq_euclidean"), mx)
+    cy = rk.cost_matrix(rk.CostSpec("euclidean"), my)
+    cfg = cntgw.make_config(0.05, n_inner=40, max_outer=6, delta_outer=1e-12)
+    out = dict(x=pc.x, y=pc.y, a=pc.a, b=pc.b)
+    for name, fn in (("kgw", rs.solve_kernel_gw), ("egw", rs.solve_entropic_gw)):
+        res = fn(cx, cy, pc.a, pc.b, cfg)
+        out.update({f"{name}__value": res.value, f"{name}__obj": np.array(res.trace.objectives),
+                    f"{name}__delta": np.array(res.trace.gamma_deltas),
+                    f"{name}__err": np.array(res.trace.marginal_errs),
+                    f"{name}__pi": res.coupling.matrix})
+    acfg = cntgw.make_config(0.05, n_inner=3, max_outer=8, delta_outer=1e-12)
+    ares = rs.solve_adaptive(rs.solve_kernel_gw, cx, cy, pc.a, pc.b, cfg=acfg)
+    out.update(ad__obj=np.array(ares.trace.objectives), ad__sched=np.array(ares.schedule))
+    return out
+
+
 GENS = {
     "c1_solve": gen_c1,
     "c4law_solve": lambda: gen_law("C4", 1024, configs.C4_EPS, dict(n_inner=100), 10),
@@ -405,6 +430,7 @@ GENS = {
     "gradients": gen_gradients,
     "multiscale": gen_multiscale,
     "kpca": gen_kpca,
+    "dense": gen_dense,
 }
 
 
