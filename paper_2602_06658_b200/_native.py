@@ -92,8 +92,9 @@ SIGNATURES = {
     "cntgw_graph_destroy": (c_int, [c_vp]),
     "cntgw_cost_product": (c_int, [c_int, c_double, c_vp, c_i64, c_int, c_vp, c_vp, c_int, c_vp, c_vp]),
     "cntgw_km_draw_workspace": (c_size_t, [c_i64, c_int]),
-    "cntgw_km_draw": (c_int, [c_vp, c_vp, c_i64, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_size_t, c_vp]),
-    "cntgw_km_update_d2": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_int, c_vp]),
+    "cntgw_km_draw": (c_int, [c_vp, c_vp, c_i64, c_vp, c_int, c_vp, c_vp, c_int, c_vp, c_vp, c_vp,
+                              c_vp, c_size_t, c_vp]),
+    "cntgw_km_update_d2": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
     "cntgw_km_assign": (c_int, [c_vp, c_i64, c_int, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "cntgw_km_centers": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
 }

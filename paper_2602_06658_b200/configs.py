@@ -65,6 +65,20 @@ def _sphere(rng, n: int) -> np.ndarray:
 
 
 def _max_sq_pair(p: np.ndarray) -> float:
+    """Largest pairwise squared distance. O(n^2): numpy up to 50k points (the
+    sizes with golden vectors), blocked fp64 on the GPU above that (C1/C3-law
+    clouds at 1e5-1e6 points would take hours on the host)."""
+    if p.shape[0] > 50_000:
+        import torch
+
+        if torch.cuda.is_available():
+            t = torch.as_tensor(p, dtype=torch.float64, device="cuda")
+            sqt = (t * t).sum(1)
+            best = 0.0
+            for i0 in range(0, t.shape[0], 1024):
+                blk = sqt[i0:i0 + 1024, None] + sqt[None, :] - 2.0 * t[i0:i0 + 1024] @ t.t()
+                best = max(best, float(blk.max()))
+            return best
     sq = (p**2).sum(axis=1)
     best = 0.0
     for i0 in range(0, p.shape[0], 2048):

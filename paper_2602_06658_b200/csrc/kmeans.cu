@@ -10,7 +10,11 @@
 //     cdf /= cdf[-1], first index with cdf > u (u drawn on the host from the
 //     same Generator). The cdf is scanned in parallel; a draw whose u falls
 //     within the rounding band of a boundary is redone by the exact
-//     sequential pass (rare: ~n * 1e-16 per draw);
+//     sequential pass for n <= kExactMaxN (a single-thread pass costs ~50 ns
+//     per element). Above that — sizes the reference's dense N x k x D
+//     k-means cannot run — the parallel answer stands: it can differ from
+//     numpy's sequential cumsum only inside that band, i.e. pick a neighbour
+//     of numpy's index with probability ~n * 1e-15 per draw;
 //   * centres: sequential sum over members in index order of fl(w_i x_i)
 //     (numpy's axis-0 reduction) divided by the pairwise sum of the member
 //     weights; centre masses: sequential np.add.at order.
@@ -70,13 +74,45 @@ __device__ __forceinline__ double np_pw_leaf(int64_t n, F at) {
   return res;
 }
 
-// full numpy pairwise sum (recursive halving on multiples of 8 above 128)
+// full numpy pairwise sum (recursive halving on multiples of 8 above 128),
+// evaluated with an explicit frame stack: device recursion would run past the
+// default per-thread stack on large clusters
 template <typename F>
 __device__ double np_pw(int64_t off, int64_t n, F at) {
-  if (n <= 128) return np_pw_leaf(n, [&](int64_t i) { return at(off + i); });
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(np_pw(off, n2, at), np_pw(off + n2, n - n2, at));
+  struct Frame {
+    int64_t off, len;
+    int state;
+    double left;
+  };
+  Frame st[48];  // depth <= log2(n / 64) + 1
+  int sp = 0;
+  st[0] = {off, n, 0, 0.0};
+  double ret = 0.0;
+  while (sp >= 0) {
+    Frame& f = st[sp];
+    if (f.len <= 128) {
+      const int64_t o = f.off;
+      ret = np_pw_leaf(f.len, [&](int64_t i) { return at(o + i); });
+      --sp;
+      continue;
+    }
+    int64_t n2 = f.len / 2;
+    n2 -= n2 % 8;
+    if (f.state == 0) {  // left half first
+      f.state = 1;
+      st[sp + 1] = {f.off, n2, 0, 0.0};
+      ++sp;
+    } else if (f.state == 1) {  // then the right half
+      f.left = ret;
+      f.state = 2;
+      st[sp + 1] = {f.off + n2, f.len - n2, 0, 0.0};
+      ++sp;
+    } else {  // combine
+      ret = __dadd_rn(f.left, ret);
+      --sp;
+    }
+  }
+  return ret;
 }
 
 template <int D>
@@ -128,6 +164,7 @@ __global__ void km_assign_kernel(const double* __restrict__ x, int64_t n,
 // ---- k-means++ draw ---------------------------------------------------------
 // workspace: [leaf sums (nleaves)] [total, flag, last] [cdf (n)] [block sums (nb)]
 constexpr int kScanThreads = 256, kScanChunk = 8;
+constexpr int64_t kExactMaxN = 1 << 17;  // exact sequential fallback up to here
 constexpr int64_t kScanBlock = (int64_t)kScanThreads * kScanChunk;
 
 struct DrawWs {
@@ -141,28 +178,58 @@ __device__ __forceinline__ double mass_at(const double* w, const double* d2, int
   return d2 ? __dmul_rn(w[i], d2[i]) : w[i];
 }
 
+// one warp per leaf: lane j < 8 runs numpy's accumulator r[j] (elements j,
+// j+8, ... of the unrolled part — coalesced 64-byte rows), lane 0 combines
+// them in numpy's fixed order and adds the tail; leaves shorter than 8 are
+// summed sequentially from 0 by lane 0
 __global__ void km_leaf_kernel(const double* w, const double* d2, const int64_t* leaf_off,
                                int nleaves, double* leaf) {
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  const int l = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
   if (l >= nleaves) return;
   const int64_t o = leaf_off[l], len = leaf_off[l + 1] - o;
-  leaf[l] = np_pw_leaf(len, [&](int64_t i) { return mass_at(w, d2, o + i); });
+  if (len < 8) {
+    if (lane == 0) {
+      double r = 0.0;
+      for (int64_t i = 0; i < len; ++i) r = __dadd_rn(r, mass_at(w, d2, o + i));
+      leaf[l] = r;
+    }
+    return;
+  }
+  const int64_t body = len - (len % 8);
+  double r = 0.0;
+  if (lane < 8) {
+    r = mass_at(w, d2, o + lane);
+    for (int64_t i = 8 + lane; i < body; i += 8) r = __dadd_rn(r, mass_at(w, d2, o + i));
+  }
+  double rr[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) rr[j] = __shfl_sync(0xffffffffu, r, j);
+  if (lane == 0) {
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(rr[0], rr[1]), __dadd_rn(rr[2], rr[3])),
+                           __dadd_rn(__dadd_rn(rr[4], rr[5]), __dadd_rn(rr[6], rr[7])));
+    for (int64_t i = body; i < len; ++i) res = __dadd_rn(res, mass_at(w, d2, o + i));
+    leaf[l] = res;
+  }
 }
 
-// combine the leaves along numpy's recursion (one thread)
-__device__ double pw_combine(const double* leaf, int64_t n, int& li) {
-  if (n <= 128) return leaf[li++];
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  const double l = pw_combine(leaf, n2, li);
-  const double r = pw_combine(leaf, n - n2, li);
-  return __dadd_rn(l, r);
-}
-
-__global__ void km_total_kernel(int64_t n, DrawWs ws) {
-  int li = 0;
-  ws.scal[0] = pw_combine(ws.leaf, n, li);
-  ws.scal[1] = 0.0;
+// combine the leaves along numpy's recursion: the host lists the internal
+// nodes of the pairwise tree by height (children before parents); one block
+// evaluates a height level per step. node ids: leaves 0..L-1, internal L.. .
+__global__ void km_total_kernel(const int* tree, const int* hoff, int nh, int nleaves, DrawWs ws) {
+  double* val = ws.leaf;  // leaf sums followed by the internal nodes
+  for (int h = 0; h < nh; ++h) {
+    for (int e = hoff[h] + threadIdx.x; e < hoff[h + 1]; e += blockDim.x) {
+      const int node = tree[3 * e], l = tree[3 * e + 1], r = tree[3 * e + 2];
+      val[node] = __dadd_rn(val[l], val[r]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const int root = hoff[nh] > 0 ? tree[3 * (hoff[nh] - 1)] : 0;
+    ws.scal[0] = val[root];
+    ws.scal[1] = 0.0;
+  }
 }
 
 __device__ __forceinline__ double prob_at(const double* w, const double* d2, double total, int64_t i) {
@@ -205,17 +272,20 @@ __global__ void km_scan_kernel(const double* w, const double* d2, int64_t n, Dra
 
 // block prefixes, cdf_last, the crossing index and its ambiguity (one block):
 // binary search over the block boundaries, then the block's elements
-__global__ void km_find_kernel(int64_t n, int nb, const double* u_all, int j, DrawWs ws,
+__global__ void km_find_kernel(int64_t n, int nb, const double* u_all, const int* jp, DrawWs ws,
                                int64_t* out_idx) {
   __shared__ double s_last;
   __shared__ int s_blk;
   __shared__ unsigned long long found;
-  const double u = u_all[j];
+  const double u = u_all[*jp];
+  extern __shared__ double sb[];  // block sums staged in parallel
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) sb[b] = ws.bsum[b];
+  __syncthreads();
   if (threadIdx.x == 0) {
     double acc = 0.0;
     for (int b = 0; b < nb; ++b) {
-      const double v = ws.bsum[b];
-      ws.bsum[b] = acc;  // exclusive block prefixes
+      const double v = sb[b];
+      sb[b] = acc;  // exclusive block prefixes
       acc = __dadd_rn(acc, v);
     }
     ws.scal[2] = acc;
@@ -224,7 +294,7 @@ __global__ void km_find_kernel(int64_t n, int nb, const double* u_all, int j, Dr
     int lo = 0, hi = nb - 1;  // first block whose end prefix exceeds target
     while (lo < hi) {
       const int mid = (lo + hi) / 2;
-      const double end = mid + 1 < nb ? ws.bsum[mid + 1] : acc;
+      const double end = mid + 1 < nb ? sb[mid + 1] : acc;
       if (end > target) hi = mid;
       else lo = mid + 1;
     }
@@ -234,7 +304,7 @@ __global__ void km_find_kernel(int64_t n, int nb, const double* u_all, int j, Dr
   __syncthreads();
   const double last = s_last, target = u * last;
   const int64_t b0 = (int64_t)s_blk * kScanBlock, b1 = min(n, b0 + kScanBlock);
-  const double pre = ws.bsum[s_blk];
+  const double pre = sb[s_blk];
   for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x)
     if (__dadd_rn(pre, ws.cdf[i]) > target) {
       atomicMin(&found, (unsigned long long)i);
@@ -246,10 +316,10 @@ __global__ void km_find_kernel(int64_t n, int nb, const double* u_all, int j, Dr
     const double band = 8.0 * (double)n * 1.1102230246251565e-16 * last;
     bool amb = idx >= n;
     if (!amb) {
-      const double v = __dadd_rn(ws.bsum[idx / kScanBlock], ws.cdf[idx]);
+      const double v = __dadd_rn(sb[idx / kScanBlock], ws.cdf[idx]);
       amb = fabs(v - target) <= band;
       if (idx > 0) {
-        const double p = __dadd_rn(ws.bsum[(idx - 1) / kScanBlock], ws.cdf[idx - 1]);
+        const double p = __dadd_rn(sb[(idx - 1) / kScanBlock], ws.cdf[idx - 1]);
         amb = amb || fabs(p - target) <= band;
       }
     }
@@ -260,9 +330,9 @@ __global__ void km_find_kernel(int64_t n, int nb, const double* u_all, int j, Dr
 
 // exact numpy semantics when the parallel scan could not decide (one thread)
 __global__ void km_exact_kernel(const double* w, const double* d2, int64_t n, const double* u_all,
-                                int j, DrawWs ws, int64_t* out_idx) {
+                                const int* jp, DrawWs ws, int64_t* out_idx) {
   if (ws.scal[1] == 0.0) return;
-  const double total = ws.scal[0], u = u_all[j];
+  const double total = ws.scal[0], u = u_all[*jp];
   double last = 0.0;
   for (int64_t i = 0; i < n; ++i) last = i == 0 ? prob_at(w, d2, total, 0) : __dadd_rn(last, prob_at(w, d2, total, i));
   double c = 0.0;
@@ -279,7 +349,8 @@ __global__ void km_exact_kernel(const double* w, const double* d2, int64_t n, co
 
 template <int D>
 __global__ void km_d2_kernel(const double* __restrict__ x, int64_t n, const int64_t* idx_dev,
-                             double* center_out, double* d2, int first) {
+                             double* centers, const int* jp, double* d2, int first) {
+  double* center_out = centers + (int64_t)(*jp) * D;
   const int64_t c = *idx_dev;
   double cc[D];
 #pragma unroll
@@ -290,6 +361,8 @@ __global__ void km_d2_kernel(const double* __restrict__ x, int64_t n, const int6
   const double v = sq_dist<D>(x + i * D, cc);
   d2[i] = first ? v : fmin(d2[i], v);
 }
+
+__global__ void km_advance_kernel(int* jp) { *jp += 1; }
 
 // ---- centres from member lists (CSR in index order) ------------------------
 template <int D>
@@ -339,40 +412,47 @@ extern "C" {
 
 size_t cntgw_km_draw_workspace(int64_t n, int nleaves) {
   const int64_t nb = (n + kScanBlock - 1) / kScanBlock;
-  return sizeof(double) * (size_t)(nleaves + 4 + n + nb);
+  // leaves + internal nodes (nleaves - 1) + scalars + cdf + block sums
+  return sizeof(double) * (size_t)(2 * nleaves + 4 + n + nb);
 }
 
 int cntgw_km_draw(const double* w, const double* d2, int64_t n, const int64_t* leaf_off,
-                  int nleaves, const double* u, int j, int64_t* out_idx, void* workspace,
-                  size_t workspace_bytes, void* stream) {
-  if (!w || !leaf_off || !u || !out_idx || n < 1 || nleaves < 1 || j < 0)
+                  int nleaves, const int* tree, const int* hoff, int nh, const double* u, const int* jp,
+                  int64_t* out_idx, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!w || !leaf_off || !tree || !hoff || !u || !out_idx || !jp || n < 1 || nleaves < 1 || nh < 0)
     return fail(CNTGW_EINVAL, "km_draw: bad arguments");
   if (!workspace || workspace_bytes < cntgw_km_draw_workspace(n, nleaves))
     return fail(CNTGW_ENOSPACE, "km_draw: workspace too small");
   const int nb = (int)((n + kScanBlock - 1) / kScanBlock);
   double* p = static_cast<double*>(workspace);
-  DrawWs ws{p, p + nleaves, p + nleaves + 4, p + nleaves + 4 + n};
+  double* after = p + 2 * nleaves;
+  DrawWs ws{p, after, after + 4, after + 4 + n};
   cudaStream_t s = as_stream(stream);
-  km_leaf_kernel<<<(nleaves + 255) / 256, 256, 0, s>>>(w, d2, leaf_off, nleaves, ws.leaf);
-  km_total_kernel<<<1, 1, 0, s>>>(n, ws);
+  km_leaf_kernel<<<(nleaves + 7) / 8, 256, 0, s>>>(w, d2, leaf_off, nleaves, ws.leaf);
+  km_total_kernel<<<1, 1024, 0, s>>>(tree, hoff, nh, nleaves, ws);
   km_scan_kernel<<<nb, kScanThreads, 0, s>>>(w, d2, n, ws);
-  km_find_kernel<<<1, 1024, 0, s>>>(n, nb, u, j, ws, out_idx);
-  km_exact_kernel<<<1, 1, 0, s>>>(w, d2, n, u, j, ws, out_idx);
+  if ((size_t)nb * sizeof(double) > 200 * 1024)
+    return fail(CNTGW_EINVAL, "km_draw: n = %lld too large for the block-sum stage", (long long)n);
+  if (nb * sizeof(double) > 48 * 1024)
+    cudaFuncSetAttribute(km_find_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  km_find_kernel<<<1, 1024, (size_t)nb * sizeof(double), s>>>(n, nb, u, jp, ws, out_idx);
+  if (n <= kExactMaxN) km_exact_kernel<<<1, 1, 0, s>>>(w, d2, n, u, jp, ws, out_idx);
   return check_launch("km_draw");
 }
 
-int cntgw_km_update_d2(const double* x, int64_t n, int d, const int64_t* idx, double* center_out,
+int cntgw_km_update_d2(const double* x, int64_t n, int d, const int64_t* idx, double* centers, int* jp,
                        double* d2, int first, void* stream) {
-  if (!x || !idx || !center_out || !d2 || n < 1) return fail(CNTGW_EINVAL, "km_update_d2: bad arguments");
+  if (!x || !idx || !centers || !jp || !d2 || n < 1) return fail(CNTGW_EINVAL, "km_update_d2: bad arguments");
   if (!dim_ok(d)) return fail(CNTGW_EINVAL, "km_update_d2: unsupported dimension %d", d);
   const unsigned blocks = (unsigned)((n + 255) / 256);
   cudaStream_t s = as_stream(stream);
   switch (d) {
 #define DCASE(V) \
-  case V: km_d2_kernel<V><<<blocks, 256, 0, s>>>(x, n, idx, center_out, d2, first); break;
+  case V: km_d2_kernel<V><<<blocks, 256, 0, s>>>(x, n, idx, centers, jp, d2, first); break;
     KM_DIMS(DCASE)
 #undef DCASE
   }
+  km_advance_kernel<<<1, 1, 0, s>>>(jp);  // next draw index (graph-replayable sequence)
   return check_launch("km_update_d2");
 }
 

@@ -15,6 +15,8 @@ from __future__ import annotations
 
 import heapq
 import math
+import os
+import time
 from dataclasses import replace
 
 import numpy as np
@@ -24,28 +26,55 @@ from . import engine
 from ._native import LIB, call
 from .kernels import EmbeddedMeasure
 
-_LEAVES: dict[int, torch.Tensor] = {}
+_TREES: dict = {}
 
 
-def _pw_leaves(n: int, device) -> torch.Tensor:
-    """Leaf offsets of numpy's pairwise summation of n values (blocks <= 128,
-    halves rounded down to multiples of 8)."""
+def _pw_tree(n: int, device):
+    """numpy's pairwise-summation tree of n values: leaf offsets (blocks <= 128,
+    halves rounded down to multiples of 8) and the internal nodes as
+    (node, left, right) ordered by height, so a level only reads finished
+    children."""
     key = (n, str(device))
-    if key not in _LEAVES:
-        offs = []
-        stack = [(0, n)]
-        while stack:  # in-order traversal (left half first)
-            off, m = stack.pop()
+    if key not in _TREES:
+        offs, nodes = [], []  # nodes: (height, left, right) with child ids
+
+        def build(off, m):  # returns (node id or ('leaf', k), height)
             if m <= 128:
                 offs.append(off)
-                continue
+                return ("L", len(offs) - 1), 0
             m2 = m // 2
             m2 -= m2 % 8
-            stack.append((off + m2, m - m2))
-            stack.append((off, m2))
+            left, hl = build(off, m2)
+            right, hr = build(off + m2, m - m2)
+            nodes.append((max(hl, hr) + 1, left, right))
+            return ("I", len(nodes) - 1), max(hl, hr) + 1
+
+        import sys
+
+        sys.setrecursionlimit(max(10000, sys.getrecursionlimit()))
+        build(0, n)
+        nleaves = len(offs)
+        order = sorted(range(len(nodes)), key=lambda t: (nodes[t][0], t))
+        ident = {t: nleaves + r for r, t in enumerate(order)}
+
+        def ref(c):
+            return c[1] if c[0] == "L" else ident[c[1]]
+
+        tree, hoff, cur = [], [0], 1
+        for t in order:
+            h = nodes[t][0]
+            while h > cur:
+                hoff.append(len(tree) // 3)
+                cur += 1
+            tree += [ident[t], ref(nodes[t][1]), ref(nodes[t][2])]
+        hoff.append(len(tree) // 3)
+        if not nodes:
+            hoff = [0]
         offs.append(n)
-        _LEAVES[key] = torch.tensor(offs, dtype=torch.int64, device=device)
-    return _LEAVES[key]
+        _TREES[key] = (torch.tensor(offs, dtype=torch.int64, device=device),
+                       torch.tensor(tree or [0, 0, 0], dtype=torch.int32, device=device),
+                       torch.tensor(hoff, dtype=torch.int32, device=device), len(hoff) - 1)
+    return _TREES[key]
 
 
 def _stream() -> int:
@@ -122,19 +151,50 @@ def _weighted_kmeans(features, weights, k, rng, sweeps: int = 100):
     k = int(k)
     # k-means++: one Generator.choice per centre = one uniform each
     us = torch.as_tensor(rng.random(k), dtype=torch.float64, device=dev)
-    leaves = _pw_leaves(n, dev)
+    leaves, tree, hoff, nh = _pw_tree(n, dev)
     nl = leaves.numel() - 1
     ws_bytes = int(LIB.cntgw_km_draw_workspace(n, nl))
     ws = torch.empty((ws_bytes + 7) // 8, dtype=torch.float64, device=dev)
     idx = torch.empty(1, dtype=torch.int64, device=dev)
+    jdev = torch.zeros(1, dtype=torch.int32, device=dev)  # draw index, advanced on the device
     centers = torch.empty((k, d), dtype=torch.float64, device=dev)
     d2 = torch.empty(n, dtype=torch.float64, device=dev)
+
+    def draw(first):
+        st = _stream()
+        call("cntgw_km_draw", w.data_ptr(), 0 if first else d2.data_ptr(), n, leaves.data_ptr(), nl,
+             tree.data_ptr(), hoff.data_ptr(), nh, us.data_ptr(), jdev.data_ptr(), idx.data_ptr(),
+             ws.data_ptr(), ws_bytes, st)
+        call("cntgw_km_update_d2", x.data_ptr(), n, d, idx.data_ptr(), centers.data_ptr(),
+             jdev.data_ptr(), d2.data_ptr(), 1 if first else 0, st)
+
+    timing = os.environ.get("CNTGW_KM_TIMING") == "1"
+    if timing:
+        t_start = time.perf_counter()
+    draw(True)
+    # the k-1 sequential draws replay a captured chunk of draws (the index
+    # lives on the device), one graph launch per chunk
+    chunk = int(os.environ.get("CNTGW_KM_CHUNK", "64"))
+    reps, rest = divmod(k - 1, chunk) if chunk > 0 else (0, k - 1)
+    if reps:
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(chunk):
+                    draw(False)
+        torch.cuda.current_stream().wait_stream(side)
+        # capture does not execute: replay all chunks
+        for _ in range(reps):
+            g.replay()
+    for _ in range(rest):
+        draw(False)
+    if timing:
+        torch.cuda.synchronize()
+        print(f"[km] {k} k-means++ draws: {time.perf_counter() - t_start:.3f} s", flush=True)
+        t_start = time.perf_counter()
     s = _stream()
-    for j in range(k):
-        call("cntgw_km_draw", w.data_ptr(), 0 if j == 0 else d2.data_ptr(), n, leaves.data_ptr(), nl,
-             us.data_ptr(), j, idx.data_ptr(), ws.data_ptr(), ws_bytes, s)
-        call("cntgw_km_update_d2", x.data_ptr(), n, d, idx.data_ptr(), centers[j].data_ptr(),
-             d2.data_ptr(), 1 if j == 0 else 0, s)
     assign = torch.zeros(n, dtype=torch.int64, device=dev)
     new = torch.empty_like(assign)
     own = torch.empty(n, dtype=torch.float64, device=dev)
@@ -150,6 +210,9 @@ def _weighted_kmeans(features, weights, k, rng, sweeps: int = 100):
         assign.copy_(new)
         if done:
             break
+    if timing:
+        torch.cuda.synchronize()
+        print(f"[km] Lloyd sweeps: {time.perf_counter() - t_start:.3f} s", flush=True)
     counts = torch.bincount(assign, minlength=k)
     masses = torch.zeros(k, dtype=torch.float64, device=dev)
     _centers_from(x, w, assign, counts, centers, masses=masses)

@@ -331,6 +331,8 @@ def gen_multiscale():
     cases["dupes"] = (xd, np.full(24, 1.0 / 24), 6)
     x64 = (rng.standard_normal((300, 64)) * 0.7).astype(np.float32).astype(np.float64)
     cases["d64"] = (x64, np.full(300, 1.0 / 300), 20)
+    xb = (rng.standard_normal((3000, 3))).astype(np.float32).astype(np.float64)
+    cases["bigclusters"] = (xb, rng.dirichlet(np.ones(3000)), 3)  # > 128 members: pairwise recursion
     for name, (x, w, k) in cases.items():
         assign, centers, cw = rs._weighted_kmeans(x, w, k, np.random.default_rng(7))
         out.update({f"{name}__x": x, f"{name}__w": w, f"{name}__k": np.array(k),

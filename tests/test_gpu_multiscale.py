@@ -27,7 +27,7 @@ def P(cuda):
     return P
 
 
-@pytest.mark.parametrize("case", ["c1", "dirichlet", "dupes", "d64"])
+@pytest.mark.parametrize("case", ["c1", "dirichlet", "dupes", "d64", "bigclusters"])
 def test_weighted_kmeans_is_the_references(P, case):
     from paper_2602_06658_b200 import solvers
 
