@@ -83,3 +83,24 @@ def test_no_cuda_means_loud_failure():
         pytest.skip("a GPU is present")
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         engine.require_cuda()
+
+
+def test_frontend_entry_points_validate_without_gpu():
+    """k-means, cost-product and graph entry points reject bad arguments
+    before touching the device (CNTGW_EINVAL / ENOSPACE + a message)."""
+    from paper_2602_06658_b200 import _native
+
+    L = _native.LIB
+    assert L.cntgw_km_assign(None, 10, 3, None, 2, None, None, None) == -1
+    assert b"km_assign" in L.cntgw_last_error()
+    buf = (ctypes.c_double * 16)()
+    p = ctypes.cast(buf, ctypes.c_void_p)
+    assert L.cntgw_km_assign(p, 10, 7 + 3, p, 2, p, p, None) == -1  # d = 10 unsupported
+    assert b"dimension 10" in L.cntgw_last_error()
+    assert L.cntgw_km_draw(p, None, 10, p, 1, p, p, 0, p, p, p, p, 8, None) == -3  # workspace
+    assert L.cntgw_km_draw_workspace(10, 1) > 8
+    assert L.cntgw_cost_product(9, 0.0, p, 10, 2, p, p, 8, p, None) == -1
+    assert b"cost kind 9" in L.cntgw_last_error()
+    assert L.cntgw_cost_product(0, 0.0, p, 10, 2, p, p, 12, p, None) == -1
+    assert L.cntgw_km_centers(None, 3, None, None, None, 1, None, None, None, None) == -1
+    assert L.cntgw_graph_launch(None, None) == -1
