@@ -249,14 +249,20 @@ int cntgw_cost_product(int kind, double par, const double* x, int64_t n, int d, 
  * sums). Points x: n x d fp64 contiguous, d in {1..8, 16, 32, 64}.
  * k-means++ draw j: p = w (d2 == NULL) or w*d2 / pairwise_sum(w*d2) (w if the
  * sum is 0); idx = first i with cumsum(p)_i / cumsum(p)_{n-1} > u[j] (device
- * u). leaf_off: nleaves+1 offsets of numpy's pairwise-sum leaves of n. */
+ * u[*jp]). leaf_off: nleaves+1 offsets of numpy's pairwise-sum leaves of n;
+ * tree/hoff/nh: the internal nodes of numpy's pairwise recursion, level by
+ * level (nh levels, hoff[nh+1] offsets into tree, each entry a
+ * (node, left, right) id triple; leaves are 0..nleaves-1), combined in the
+ * reference's order. The draw index lives on the device (*jp) so a captured
+ * sequence of draws can be replayed. */
 size_t cntgw_km_draw_workspace(int64_t n, int nleaves);
 int cntgw_km_draw(const double* w, const double* d2, int64_t n, const int64_t* leaf_off,
-                  int nleaves, const double* u, int j, int64_t* out_idx, void* workspace,
-                  size_t workspace_bytes, void* stream);
-/* center_out = x[*idx]; d2 = |x - center|^2 (first) or min(d2, |x - center|^2) */
-int cntgw_km_update_d2(const double* x, int64_t n, int d, const int64_t* idx, double* center_out,
-                       double* d2, int first, void* stream);
+                  int nleaves, const int* tree, const int* hoff, int nh, const double* u,
+                  const int* jp, int64_t* out_idx, void* workspace, size_t workspace_bytes,
+                  void* stream);
+/* centers[*jp] = x[*idx]; d2 = |x - c|^2 (first) or min(d2, |x - c|^2); then ++*jp */
+int cntgw_km_update_d2(const double* x, int64_t n, int d, const int64_t* idx, double* centers,
+                       int* jp, double* d2, int first, void* stream);
 /* assign_i = first argmin_j |x_i - c_j|^2, own_i = that distance */
 int cntgw_km_assign(const double* x, int64_t n, int d, const double* centers, int64_t k,
                     int64_t* assign, double* own, void* stream);
