@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define CNTGW_ABI_VERSION 2
+#define CNTGW_ABI_VERSION 3
 
 typedef enum cntgw_status {
   CNTGW_OK = 0,
@@ -52,9 +52,17 @@ typedef enum cntgw_status {
   CNTGW_ENOSPACE = -3  /* workspace smaller than the *_workspace query */
 } cntgw_status;
 
-/* Exponent assembly: fp32 FFMA2, fp64 DFMA, or the tcgen05 tensor cores with a
- * 3xTF32 split (kd in {8, 16}, no sq coordinate; well-scaled problems). */
-typedef enum cntgw_precision { CNTGW_F32 = 0, CNTGW_F64 = 1, CNTGW_TF32X3 = 2 } cntgw_precision;
+/* Exponent assembly: fp32 FFMA2, fp64 DFMA, the tcgen05 tensor cores with a
+ * 3xTF32 split (kd in {8, 16}, no sq coordinate; well-scaled problems), or
+ * CNTGW_F32C: fp32 pair terms on locality-ordered, centred tiles with fp64
+ * per-tile offsets (kd + sq <= 8; the cold low-dimensional laws, see
+ * cntgw_prep_cols_ctr). */
+typedef enum cntgw_precision {
+  CNTGW_F32 = 0,
+  CNTGW_F64 = 1,
+  CNTGW_TF32X3 = 2,
+  CNTGW_F32C = 3
+} cntgw_precision;
 
 /* Device-resident state of one Sinkhorn loop (sinkhorn.py:191-258 control).
  * Lives in device memory; the host initialises it with cntgw_sweep_init and
@@ -143,6 +151,33 @@ int cntgw_sweep_apply(const cntgw_sweep_state* st, double* pot, const double* te
 int cntgw_prep_cols(const cntgw_sweep_state* st, int prec, int kd, int sq_flag, const void* feat,
                     int64_t ld, const void* sq, const double* pot, const double* log2w, int64_t m,
                     void* rec, void* stream);
+/* ---- K1/K2, CNTGW_F32C: centred fp32 on locality-ordered tiles ----------
+ * Same half-update (sinkhorn.py:166-176) for problems whose exponent terms are
+ * too large for fp32 (|t| ~ 1e6 on the C4 law) but whose points are
+ * low-dimensional. Rows and columns are visited in a locality order `order`
+ * (a permutation; NULL = identity), 128-row groups I and 256-column tiles J
+ * are centred, and with X_i = [x_i | s_i], Zr_j = [-2 lam z_j | -2 lam s_j]
+ * (expanded square, as the fp64 records) the exponent splits exactly into
+ *   q_ij = A_j^I (fp64, per group and column) + B_i^J (fp64, per row and tile)
+ *        + <dX_i, dZ_j> (fp32 FFMA2 per pair, small after centring).
+ * cntgw_locality_codes: 63-bit Morton codes of the first min(d, 3)
+ * coordinates (x: n x d fp64, stride ld; bbox: 6 doubles of scratch); the
+ * caller sorts them (stable) to obtain `order`.
+ * cntgw_prep_rows_ctr / cntgw_prep_cols_ctr fill the row block / column block
+ * (sizes from the *_bytes queries) from fp64 features in the caller's order;
+ * the column block is per half-update (it holds lam and pot). cntgw_softmin
+ * with prec = CNTGW_F32C then takes row_feat = the row block, row_sq = the
+ * rows' fp64 squared coordinate in the caller's order (or NULL without sq),
+ * col_rec = the column block; outputs are in the caller's order. */
+int cntgw_locality_codes(const double* x, int64_t n, int d, int64_t ld, double* bbox, int64_t* codes,
+                         void* stream);
+size_t cntgw_ctr_rows_bytes(int64_t n, int kd, int sq_flag);
+size_t cntgw_ctr_cols_bytes(int64_t m, int kd, int sq_flag);
+int cntgw_prep_rows_ctr(int kd, int sq_flag, const double* feat, int64_t ld, const double* sq,
+                        const int64_t* order, int64_t n, void* rows, void* stream);
+int cntgw_prep_cols_ctr(const cntgw_sweep_state* st, int kd, int sq_flag, const double* feat, int64_t ld,
+                        const double* sq, const double* pot, const double* log2w, const int64_t* order,
+                        int64_t m, void* cols, void* stream);
 /* Scratch bytes the half-update needs for split-column partials. */
 size_t cntgw_softmin_workspace(int prec, int64_t n, int64_t m, int kd, int sq_flag);
 /* out_i = row_add_i - LSE2_j(t_ij)/lam (row_add nullable => 0). If out_max and

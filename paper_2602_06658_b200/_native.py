@@ -44,7 +44,8 @@ class OuterStateStruct(ctypes.Structure):
     ]
 
 
-F32, F64, TF32X3 = 0, 1, 2  # cntgw_precision
+F32, F64, TF32X3, F32C = 0, 1, 2, 3  # cntgw_precision
+ABI_VERSION = 3  # CNTGW_ABI_VERSION
 
 # name -> (restype, argtypes); every symbol include/cntgw_b200.h declares
 SIGNATURES = {
@@ -52,6 +53,12 @@ SIGNATURES = {
     "cntgw_last_error": (ctypes.c_char_p, []),
     "cntgw_sweep_state_size": (c_int, []),
     "cntgw_col_stride": (c_int, [c_int, c_int, c_int]),
+    "cntgw_locality_codes": (c_int, [c_vp, c_i64, c_int, c_i64, c_vp, c_vp, c_vp]),
+    "cntgw_ctr_rows_bytes": (c_size_t, [c_i64, c_int, c_int]),
+    "cntgw_ctr_cols_bytes": (c_size_t, [c_i64, c_int, c_int]),
+    "cntgw_prep_rows_ctr": (c_int, [c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "cntgw_prep_cols_ctr": (c_int, [c_vp, c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,
+                                    c_vp, c_vp]),
     "cntgw_cols_padded": (c_i64, [c_i64]),
     "cntgw_sweep_init": (c_int, [c_vp, c_double, c_double, c_double, c_int, c_int, c_vp]),
     "cntgw_sweep_begin": (c_int, [c_vp, c_vp]),
@@ -115,7 +122,7 @@ def _load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.cntgw_abi_version() != 2:
+    if lib.cntgw_abi_version() != ABI_VERSION:
         raise ImportError("libcntgw_b200.so ABI version mismatch; rebuild the extension")
     if lib.cntgw_sweep_state_size() != ctypes.sizeof(SweepStateStruct):
         raise ImportError("cntgw_sweep_state layout mismatch between header and host mirror")

@@ -8,6 +8,7 @@
 
 #include "common.cuh"
 #include "softmin.cuh"
+#include "softmin_ctr.cuh"
 #include "softmin_dmma.cuh"
 #include "softmin_tc.cuh"
 #include "sweep.cuh"
@@ -165,7 +166,38 @@ KernelPick pick_tc() {
   return k;
 }
 
+// CNTGW_F32C: centred fp32 pairs over locality-ordered tiles (softmin_ctr.cuh);
+// KX = kd + sq padded to 4 (8 rows per thread) or 8 (4 rows per thread).
+template <int KX>
+KernelPick pick_ctr() {
+  constexpr int R = KX <= 4 ? 8 : 4, MINB = KX <= 4 ? 4 : 3;
+  KernelPick k;
+  // tuning alternatives (tools/ctr_check.py): CNTGW_CTR_POLY row pairs per
+  // 4-column group on the FMA-pipe exp2; CNTGW_CTR_MINB=3 trades a CTA per SM
+  // for registers
+  const int poly = env_int("CNTGW_CTR_POLY", 0), minb3 = env_int("CNTGW_CTR_MINB", MINB) == 3;
+  if (minb3)
+    k.fn = poly == 1 ? (void*)softmin_ctr_kernel<KX, R, 4, 3, 1>
+         : poly == 2 ? (void*)softmin_ctr_kernel<KX, R, 4, 3, 2>
+                     : (void*)softmin_ctr_kernel<KX, R, 4, 3, 0>;
+  else
+    k.fn = poly == 1 ? (void*)softmin_ctr_kernel<KX, R, 4, MINB, 1>
+         : poly == 2 ? (void*)softmin_ctr_kernel<KX, R, 4, MINB, 2>
+                     : (void*)softmin_ctr_kernel<KX, R, 4, MINB, 0>;
+  k.rows = R;
+  k.smem = CtrSmem<KX, R>::kBytes;
+  k.rec_bytes = (KX + 1) * sizeof(double) + KX * sizeof(float);
+  return k;
+}
+
 bool lookup(int prec, int kd, int sq, KernelPick* out) {
+  if (prec == CNTGW_F32C) {
+    if (!kd_supported(kd)) return false;
+    const int kx = kd + (sq ? 1 : 0);
+    if (kx <= 4) { *out = pick_ctr<4>(); return true; }
+    if (kx <= 8) { *out = pick_ctr<8>(); return true; }
+    return false;
+  }
   if (prec == CNTGW_TF32X3) {
     if (sq) return false;
     if (kd == 8) { *out = pick_tc<8>(); return true; }
@@ -301,6 +333,61 @@ __global__ void softmin_dense_kernel(const cntgw_sweep_state* st, int skip, cons
   if (lane == 0) out[i] = (row_add ? row_add[i] : 0.0) - (mx + log2(sm)) / lam;
 }
 
+// ---- locality order (CNTGW_F32C) ---------------------------------------------
+// Bounding box of the first d3 <= 3 coordinates (one block; O(n d3) loads).
+__global__ void __launch_bounds__(1024) bbox_kernel(const double* x, int64_t n, int d3, int64_t ld,
+                                                    double* bb) {
+  __shared__ double lo_s[3][32], hi_s[3][32];
+  double lo[3] = {CUDART_INF, CUDART_INF, CUDART_INF}, hi[3] = {-CUDART_INF, -CUDART_INF, -CUDART_INF};
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+    for (int k = 0; k < d3; ++k) {
+      const double v = x[i * ld + k];
+      lo[k] = fmin(lo[k], v);
+      hi[k] = fmax(hi[k], v);
+    }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int k = 0; k < 3; ++k) {
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[k] = fmin(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+      hi[k] = fmax(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+    }
+    if (l == 0) {
+      lo_s[k][w] = lo[k];
+      hi_s[k][w] = hi[k];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    const int k = threadIdx.x;
+    double a = CUDART_INF, b = -CUDART_INF;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+      a = fmin(a, lo_s[k][q]);
+      b = fmax(b, hi_s[k][q]);
+    }
+    bb[k] = a;
+    bb[3 + k] = b;
+  }
+}
+
+// 63-bit Morton (Z-order) code: 63/d3 bits per coordinate, bits interleaved.
+__global__ void morton_kernel(const double* x, int64_t n, int d3, int64_t ld, const double* bb,
+                              int64_t* codes) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int bits = 63 / d3;
+  const double top = (double)((1ULL << bits) - 1);
+  uint64_t q[3] = {0, 0, 0};
+  for (int k = 0; k < d3; ++k) {
+    const double span = bb[3 + k] - bb[k];
+    const double u = span > 0.0 ? (x[i * ld + k] - bb[k]) / span : 0.0;
+    q[k] = (uint64_t)fmin(fmax(u * top, 0.0), top);
+  }
+  uint64_t c = 0;
+  for (int b = bits - 1; b >= 0; --b)
+    for (int k = 0; k < d3; ++k) c = (c << 1) | ((q[k] >> b) & 1ULL);
+  codes[i] = (int64_t)c;
+}
+
 }  // namespace
 
 // ================================================================================
@@ -317,6 +404,11 @@ int cntgw_col_stride(int prec, int kd, int sq) {
   if (prec == CNTGW_F64) {
     const int vec = (raw + 1) / 2 * 2, k4 = (kd + (sq ? 1 : 0) + 3) / 4 * 4;
     return k4 > vec ? k4 : vec;
+  }
+  if (prec == CNTGW_F32C) {
+    const int kx = kd + (sq ? 1 : 0);
+    if (kx > 8) return fail(CNTGW_EINVAL, "centred fp32 path supports kd + sq <= 8 (kd=%d sq=%d)", kd, sq);
+    return kx <= 4 ? 4 : 8;  // fp32 dZ floats per column (see cntgw_ctr_cols_bytes for the block)
   }
   if (prec == CNTGW_TF32X3) {
     if (sq || (kd != 8 && kd != 16))
@@ -374,6 +466,7 @@ int cntgw_prep_cols(const cntgw_sweep_state* st, int prec, int kd, int sq_flag, 
                     void* rec, void* stream) {
   if (!st || !feat || !log2w || !rec || m < 1) return fail(CNTGW_EINVAL, "prep_cols: bad arguments");
   if (sq_flag && !sq) return fail(CNTGW_EINVAL, "prep_cols: sq_flag set without sq values");
+  if (prec == CNTGW_F32C) return fail(CNTGW_EINVAL, "prep_cols: CNTGW_F32C columns are packed by cntgw_prep_cols_ctr");
   const int stride = cntgw_col_stride(prec, kd, sq_flag);
   if (stride < 0) return stride;
   const int64_t mpad = cntgw_cols_padded(m);
@@ -398,6 +491,66 @@ int cntgw_prep_cols(const cntgw_sweep_state* st, int prec, int kd, int sq_flag, 
         st, kd, sqf, stride, static_cast<const double*>(feat), ld, static_cast<const double*>(sq),
         pot, log2w, m, mpad, static_cast<double*>(rec));
   return check_launch("prep_cols");
+}
+
+int cntgw_locality_codes(const double* x, int64_t n, int d, int64_t ld, double* bbox, int64_t* codes,
+                         void* stream) {
+  if (!x || !bbox || !codes || n < 1 || d < 1 || ld < d) return fail(CNTGW_EINVAL, "locality_codes: bad arguments");
+  const int d3 = d < 3 ? d : 3;
+  cudaStream_t s = as_stream(stream);
+  bbox_kernel<<<1, 1024, 0, s>>>(x, n, d3, ld, bbox);
+  morton_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, n, d3, ld, bbox, codes);
+  return check_launch("locality_codes");
+}
+
+static int ctr_kx(int kd, int sq_flag) {
+  if (!kd_supported(kd)) return -1;
+  const int kx = kd + (sq_flag ? 1 : 0);
+  return kx <= 4 ? 4 : (kx <= 8 ? 8 : -1);
+}
+
+size_t cntgw_ctr_rows_bytes(int64_t n, int kd, int sq_flag) {
+  const int kx = ctr_kx(kd, sq_flag);
+  return (kx < 0 || n < 1) ? 0 : ctr_rows_bytes(n, kx);
+}
+
+size_t cntgw_ctr_cols_bytes(int64_t m, int kd, int sq_flag) {
+  const int kx = ctr_kx(kd, sq_flag);
+  return (kx < 0 || m < 1) ? 0 : ctr_cols_bytes(cntgw_cols_padded(m), kx);
+}
+
+int cntgw_prep_rows_ctr(int kd, int sq_flag, const double* feat, int64_t ld, const double* sq,
+                        const int64_t* order, int64_t n, void* rows, void* stream) {
+  if (!feat || !rows || n < 1 || ld < kd) return fail(CNTGW_EINVAL, "prep_rows_ctr: bad arguments");
+  if (sq_flag && !sq) return fail(CNTGW_EINVAL, "prep_rows_ctr: sq_flag set without sq values");
+  const int kx = ctr_kx(kd, sq_flag);
+  if (kx < 0) return fail(CNTGW_EINVAL, "prep_rows_ctr: kd + sq = %d + %d > 8", kd, sq_flag);
+  const unsigned g = (unsigned)ctr_groups(n);
+  cudaStream_t s = as_stream(stream);
+  if (kx == 4)
+    prep_rows_ctr_kernel<4><<<g, kCtrRowGroup, 0, s>>>(kd, sq_flag ? 1 : 0, feat, ld, sq, order, n, rows);
+  else
+    prep_rows_ctr_kernel<8><<<g, kCtrRowGroup, 0, s>>>(kd, sq_flag ? 1 : 0, feat, ld, sq, order, n, rows);
+  return check_launch("prep_rows_ctr");
+}
+
+int cntgw_prep_cols_ctr(const cntgw_sweep_state* st, int kd, int sq_flag, const double* feat, int64_t ld,
+                        const double* sq, const double* pot, const double* log2w, const int64_t* order,
+                        int64_t m, void* cols, void* stream) {
+  if (!st || !feat || !log2w || !cols || m < 1 || ld < kd)
+    return fail(CNTGW_EINVAL, "prep_cols_ctr: bad arguments");
+  if (sq_flag && !sq) return fail(CNTGW_EINVAL, "prep_cols_ctr: sq_flag set without sq values");
+  const int kx = ctr_kx(kd, sq_flag);
+  if (kx < 0) return fail(CNTGW_EINVAL, "prep_cols_ctr: kd + sq = %d + %d > 8", kd, sq_flag);
+  const int64_t mpad = cntgw_cols_padded(m);
+  const unsigned tiles = (unsigned)(mpad / kColTile);
+  cudaStream_t s = as_stream(stream);
+  const int sqf = sq_flag ? 1 : 0;
+  if (kx == 4)
+    prep_cols_ctr_kernel<4><<<tiles, kColTile, 0, s>>>(st, kd, sqf, feat, ld, sq, pot, log2w, order, m, mpad, cols);
+  else
+    prep_cols_ctr_kernel<8><<<tiles, kColTile, 0, s>>>(st, kd, sqf, feat, ld, sq, pot, log2w, order, m, mpad, cols);
+  return check_launch("prep_cols_ctr");
 }
 
 size_t cntgw_softmin_workspace(int prec, int64_t n, int64_t m, int kd, int sq_flag) {
@@ -434,6 +587,10 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
   a.out = out;
   a.out_max = out_max;
   a.out_sum = out_sum;
+  {  // fp32 pair-term bound per (row group, column tile) of CNTGW_F32C, log2 units
+    const char* e = getenv("CNTGW_CTR_TILE_LIMIT");
+    a.ctr_limit = e ? atof(e) : 65536.0;
+  }
   if (p.nchunks > 1) {
     const size_t need = plan_workspace(p, n);
     if (workspace == nullptr || workspace_bytes < need)

@@ -48,6 +48,7 @@ struct SoftminArgs {
   double* out_sum;
   double* part_max;  // [nchunks][n] split-column partials (nchunks > 1)
   double* part_sum;
+  double ctr_limit;  // CNTGW_F32C: per-(group, tile) bound on the fp32 pair term
 };
 
 template <typename T, int KD, int SQ>
@@ -410,7 +411,8 @@ static __global__ void lse_combine_kernel(const cntgw_sweep_state* st, int skip,
     out_max[i] = mx;
     out_sum[i] = sm;
   } else {
-    const double inv_lam = prec == CNTGW_F64 ? 1.0 / st->lam_d : 1.0 / (double)st->lam;
+    const double inv_lam =
+        (prec == CNTGW_F64 || prec == CNTGW_F32C) ? 1.0 / st->lam_d : 1.0 / (double)st->lam;
     out[i] = (row_add ? row_add[i] : 0.0) - (mx + log2(sm)) * inv_lam;
   }
 }

@@ -29,7 +29,7 @@ import numpy as np
 import torch
 
 from . import _native
-from ._native import F32, F64, LIB, TF32X3, SweepStateStruct, call
+from ._native import F32, F32C, F64, LIB, TF32X3, SweepStateStruct, call
 
 SUPPORTED_KD = (1, 2, 3, 4, 8, 16, 32, 64)
 # fp32 exponent assembly is used while lam * (term magnitudes) stays below this
@@ -99,13 +99,86 @@ def exponent_scale(eps: float, feat_r, sq_r, feat_c, sq_c, pot_abs: float = 0.0)
     return lam * (pot_abs + dot + sq)
 
 
+# CNTGW_F32C (centred fp32 on locality-ordered tiles): a (row group, column
+# tile) pair whose fp32 pair term can exceed this bound (log2 units; fp32 ulp
+# there is 2^-8) runs in fp64 inside the kernel (CNTGW_CTR_TILE_LIMIT, read
+# by the library); the path is chosen for a cold problem while at most
+# CTR_MAX_DEFERRED of the pairs need that fallback (softmin_ctr.cuh).
+CTR_TILE_LIMIT = float(os.environ.get("CNTGW_CTR_TILE_LIMIT", 65536.0))
+CTR_MAX_DEFERRED = 0.05
+CTR_ROW_GROUP, CTR_COL_TILE = 128, 256
+
+
+def ctr_supported(kd: int, sq: bool) -> bool:
+    return kd + int(bool(sq)) <= 8
+
+
+def locality_order(coords: torch.Tensor) -> torch.Tensor:
+    """Permutation visiting the points in Morton (Z-curve) order of their first
+    min(d, 3) coordinates (cntgw_locality_codes + a stable device sort)."""
+    x = coords.to(torch.float64)
+    if x.ndim == 1:
+        x = x[:, None]
+    x = x.contiguous()
+    n, d = x.shape
+    codes = torch.empty(n, dtype=torch.int64, device=x.device)
+    bbox = torch.empty(6, dtype=torch.float64, device=x.device)
+    call("cntgw_locality_codes", x.data_ptr(), n, d, d, bbox.data_ptr(), codes.data_ptr(), _stream())
+    return torch.sort(codes, stable=True).indices
+
+
+def _tile_radii(pts: torch.Tensor, order: torch.Tensor, tile: int) -> torch.Tensor:
+    """max |p - mean| of each consecutive `tile`-point group in `order`."""
+    p = pts[order]
+    n = p.shape[0]
+    full = n // tile * tile
+    out = []
+    if full:
+        g = p[:full].view(-1, tile, p.shape[1])
+        out.append((g - g.mean(1, keepdim=True)).norm(dim=2).amax(1))
+    if full < n:
+        t = p[full:]
+        out.append((t - t.mean(0, keepdim=True)).norm(dim=1).amax()[None])
+    return torch.cat(out)
+
+
+def _side_points(side) -> torch.Tensor:
+    return side.feat64 if side.sq64 is None else torch.cat([side.feat64, side.sq64[:, None]], 1)
+
+
+def centred_radii(eps: float, rows: "Side", cols: "Side"):
+    """(group radii of the rows, tile radii of the columns in log2-scaled units):
+    their product bounds the fp32 pair term of a (group, tile) pair."""
+    lam = math.log2(math.e) / eps
+    rr = _tile_radii(_side_points(rows), rows.locality(), CTR_ROW_GROUP)
+    rc = _tile_radii(_side_points(cols), cols.locality(), CTR_COL_TILE) * (2.0 * lam)
+    return rr, rc
+
+
+def centred_scale(eps: float, rows: "Side", cols: "Side") -> float:
+    """Worst (group, tile) bound of the fp32 pair term (diagnostic)."""
+    rr, rc = centred_radii(eps, rows, cols)
+    return float(rr.max() * rc.max())
+
+
+def centred_deferred_fraction(eps: float, rows: "Side", cols: "Side") -> float:
+    """Fraction of (row group, column tile) pairs the kernel will run in fp64."""
+    rr, rc = centred_radii(eps, rows, cols)
+    rc_sorted = torch.sort(rc).values
+    need = CTR_TILE_LIMIT / rr.clamp_min(1e-300)  # a tile is deferred when rc > need
+    over = rc_sorted.numel() - torch.searchsorted(rc_sorted, need, right=True)
+    return float(over.sum()) / (rr.numel() * rc.numel())
+
+
 def tc_supported(kd: int, sq: bool) -> bool:
     """Shapes the tcgen05 3xTF32 half-update serves (include/cntgw_b200.h)."""
     return kd in (8, 16) and not sq
 
 
-def choose_precision(scale: float, kd: int = 0, sq: bool = True) -> int:
-    """fp64 for cold problems; otherwise the tensor cores where the shape allows."""
+def choose_precision(scale: float, kd: int = 0, sq: bool = True, ctr_deferred=None) -> int:
+    """Cold problems: the centred fp32 path while few tile pairs need its fp64
+    fallback (``ctr_deferred``, a callable evaluated only then), else fp64;
+    otherwise the tensor cores where the shape allows."""
     forced = os.environ.get("CNTGW_PRECISION", "auto").lower()
     if forced in ("f32", "fp32"):
         return F32
@@ -113,7 +186,12 @@ def choose_precision(scale: float, kd: int = 0, sq: bool = True) -> int:
         return F64
     if forced in ("tc", "tf32x3"):
         return TF32X3 if tc_supported(kd, sq) else F32
+    if forced in ("f32c", "ctr"):
+        return F32C if ctr_supported(kd, sq) else F64
     if scale >= F32_EXPONENT_LIMIT:
+        if (ctr_deferred is not None and ctr_supported(kd, sq)
+                and os.environ.get("CNTGW_CTR", "1") != "0" and ctr_deferred() <= CTR_MAX_DEFERRED):
+            return F32C
         return F64
     return TF32X3 if tc_supported(kd, sq) else F32
 
@@ -147,12 +225,19 @@ class Side:
     squared-difference coordinate, weights. fp64 is the source of truth; the
     fp32 copies feed the fp32 kernels."""
 
-    def __init__(self, feat64: torch.Tensor, sq64: torch.Tensor | None, w: torch.Tensor):
+    def __init__(self, feat64: torch.Tensor, sq64: torch.Tensor | None, w: torch.Tensor,
+                 order: torch.Tensor | None = None):
         self.feat64 = feat64
         self.sq64 = sq64
         self.w = w
         self.log2w = torch.log2(w)
         self._f32 = None
+        self.order = order  # locality order of the points (CNTGW_F32C), lazily from feat64
+
+    def locality(self) -> torch.Tensor:
+        if self.order is None:
+            self.order = locality_order(_side_points(self))
+        return self.order
 
     @staticmethod
     def make(feat, sq, w, device, kd):
@@ -203,12 +288,24 @@ class HalfUpdate:
             rec_bytes = max(rec_bytes, stride * (8 if p == F64 else 4))
         self.rec = torch.empty(LIB.cntgw_cols_padded(cols.n) * rec_bytes // 8, dtype=torch.float64,
                                device=dev)
+        if ctr_supported(self.kd, self.sq):
+            precs = precs + (F32C,)
+            # row / column blocks of the centred path (fixed addresses for graph capture)
+            self.ctr_rows = torch.empty(int(LIB.cntgw_ctr_rows_bytes(rows.n, self.kd, int(self.sq))),
+                                        dtype=torch.uint8, device=dev)
+            self.ctr_cols = torch.empty(int(LIB.cntgw_ctr_cols_bytes(cols.n, self.kd, int(self.sq))),
+                                        dtype=torch.uint8, device=dev)
         wsb = max(LIB.cntgw_softmin_workspace(p, rows.n, cols.n, self.kd, int(self.sq)) for p in precs)
         self.ws = torch.empty(max(int(wsb), 16), dtype=torch.uint8, device=dev)
 
     def pack(self, state: SweepState, pot_cols: torch.Tensor | None, prec=None):
         prec = self.prec if prec is None else prec
         c = self.cols
+        if prec == F32C:
+            call("cntgw_prep_cols_ctr", state.ptr, self.kd, int(self.sq), c.feat64.data_ptr(), self.kd,
+                 _p(c.sq64 if self.sq else None), _p(pot_cols), c.log2w.data_ptr(),
+                 c.locality().data_ptr(), c.n, self.ctr_cols.data_ptr(), _stream())
+            return
         feat, sq = c.feat(prec)
         call("cntgw_prep_cols", state.ptr, prec, self.kd, int(self.sq), feat.data_ptr(), self.kd,
              _p(sq), _p(pot_cols), c.log2w.data_ptr(), c.n, self.rec.data_ptr(), _stream())
@@ -216,9 +313,16 @@ class HalfUpdate:
     def stream(self, state: SweepState, out=None, skip=True, row_add=None, out_max=None,
                out_sum=None):
         r = self.rows
-        feat, sq = r.feat(self.prec)
+        if self.prec == F32C:
+            sq = r.sq64 if self.sq else None
+            call("cntgw_prep_rows_ctr", self.kd, int(self.sq), r.feat64.data_ptr(), self.kd, _p(sq),
+                 r.locality().data_ptr(), r.n, self.ctr_rows.data_ptr(), _stream())
+            feat, rec = self.ctr_rows, self.ctr_cols
+        else:
+            feat, sq = r.feat(self.prec)
+            rec = self.rec
         call("cntgw_softmin", state.ptr, int(skip), self.prec, self.kd, int(self.sq),
-             feat.data_ptr(), self.kd, _p(sq), _p(row_add), self.rec.data_ptr(), r.n, self.cols.n,
+             feat.data_ptr(), self.kd, _p(sq), _p(row_add), rec.data_ptr(), r.n, self.cols.n,
              _p(out), _p(out_max), _p(out_sum), self.ws.data_ptr(), self.ws.numel(), _stream())
 
     def __call__(self, state, pot_cols, out, skip=True, row_add=None):

@@ -244,7 +244,10 @@ def _set_precision(problem, eps, f0, g0):
               float(np.abs(g0 - problem.col_sep).max(initial=0.0)))
     scale = engine.exponent_scale(eps, fwd.rows.feat64, fwd.rows.sq64, fwd.cols.feat64,
                                   fwd.cols.sq64, pot)
-    prec = engine.choose_precision(scale, fwd.kd, fwd.sq)
+    prec = engine.choose_precision(scale, fwd.kd, fwd.sq,
+                                   ctr_deferred=lambda: max(
+                                       engine.centred_deferred_fraction(eps, fwd.rows, fwd.cols),
+                                       engine.centred_deferred_fraction(eps, fwd.cols, fwd.rows)))
     problem.fwd.prec = prec
     problem.bwd.prec = prec
 

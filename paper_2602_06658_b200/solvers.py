@@ -203,8 +203,10 @@ class _GwDevice:
         else:
             rows_feat = engine.to_dev64(x, device, self.kd)
             cols_feat = torch.zeros(self.m, self.kd, dtype=torch.float64, device=device)
-        self.src = engine.Side(rows_feat, self.sx, self.a)
-        self.tgt = engine.Side(cols_feat, self.ty, self.b)
+        # locality orders of the point clouds (CNTGW_F32C tiles); the Gamma-dependent
+        # features stay coherent along them (|Gamma dY| <= |Gamma| |dY|)
+        self.src = engine.Side(rows_feat, self.sx, self.a, order=engine.locality_order(self.x))
+        self.tgt = engine.Side(cols_feat, self.ty, self.b, order=engine.locality_order(self.y))
         self.fwd = engine.HalfUpdate(self.src, self.tgt, True)
         self.bwd = engine.HalfUpdate(self.tgt, self.src, True)
         self.loop = engine.SinkhornLoop(self.fwd, self.bwd, self.a, self.b, device, comm=self.comm)
@@ -293,8 +295,18 @@ class _GwDevice:
             tdist.all_reduce(fmax, op=tdist.ReduceOp.MAX)
         pot = float(torch.maximum(fmax, g.abs().max()))
         scale = engine.exponent_scale(eps_min, self.src.feat64, self.sx, self.tgt.feat64, self.ty, pot)
-        self.prec = engine.choose_precision(scale, self.kd, True)
+        self.prec = engine.choose_precision(
+            scale, self.kd, True, ctr_deferred=lambda: self._ctr_deferred(eps_min))
         self.loop.set_precision(self.prec)
+
+    def _ctr_deferred(self, eps_min):
+        s = max(engine.centred_deferred_fraction(eps_min, self.src, self.tgt),
+                engine.centred_deferred_fraction(eps_min, self.tgt, self.src))
+        if self.comm is not None:  # every rank must pick the same path
+            t = torch.tensor([s], dtype=torch.float64, device=self.device)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            s = float(t)
+        return s
 
     # -- one outer step ------------------------------------------------------
     def step(self, f, g, gamma: np.ndarray, loop_cfg: engine.LoopConfig, eps_outer: float,

@@ -50,11 +50,13 @@ def _half_update(env, cost, a, b, g, eps, prec=None):
     return out.cpu().numpy() + prob.row_sep
 
 
-@pytest.mark.parametrize("prec", [0, 1], ids=["f32", "f64"])
+@pytest.mark.parametrize("prec", [0, 1, 3], ids=["f32", "f64", "f32c"])
 @pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 8, 16, 17, 33, 64, 65])
 @pytest.mark.parametrize("n,m", [(1, 1), (1, 300), (300, 1), (129, 257), (1000, 1000), (2049, 771)])
 def test_sq_euclidean_half_update(env, k, n, m, prec):
     P, engine, S, O, torch, dev = env
+    if prec == 3 and not engine.ctr_supported(engine.padded_kd(max(k - 1, 1)), True):
+        pytest.skip("centred fp32 path: kd + sq <= 8")
     rng = np.random.default_rng(k * 1000 + n + m)
     x = rng.standard_normal((n, k)) * 0.5
     z = rng.standard_normal((m, k)) * 0.5
@@ -66,7 +68,7 @@ def test_sq_euclidean_half_update(env, k, n, m, prec):
     eps = 0.05
     got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, prec)
     want = O.softmin(O.SqEuclid(x, z), np.log(b), g, eps)
-    assert _rel(got, want) < (1e-5 if prec == 0 else 5e-7)
+    assert _rel(got, want) < (5e-7 if prec == 1 else 1e-5)
 
 
 @pytest.mark.parametrize("k", [4, 16])
@@ -82,7 +84,7 @@ def test_low_rank_half_update(env, k):
     assert _rel(got, want) < 1e-5
 
 
-@pytest.mark.parametrize("prec", [0, 1], ids=["f32", "f64"])
+@pytest.mark.parametrize("prec", [0, 1, 3], ids=["f32", "f64", "f32c"])
 def test_rebase_path_under_huge_exponents(env, prec):
     """Cold regime: |exponent| ~ 1e6 log2 units; exercises lazy rebasing."""
     P, engine, S, O, torch, dev = env
@@ -94,7 +96,53 @@ def test_rebase_path_under_huge_exponents(env, prec):
     eps = 1.25e-3
     got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, prec)
     want = O.softmin(O.SqEuclid(x, z), np.log(b), g, eps)
-    assert _rel(got, want) < (1e-5 if prec == 0 else 5e-7)
+    assert _rel(got, want) < (5e-7 if prec == 1 else 1e-5)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+@pytest.mark.parametrize("n,m", [(5000, 7000), (130, 100_000)])
+def test_centred_path_cold_locality(env, k, n, m):
+    """CNTGW_F32C on a cold clustered law (|exponent| ~ 1e5-1e6 log2 units,
+    where plain fp32 loses ~0.1 log2 units per term): fp32 pair terms on
+    Morton-ordered centred tiles match the fp64 oracle; outputs come back in
+    the caller's (unsorted) order."""
+    P, engine, S, O, torch, dev = env
+    rng = np.random.default_rng(10 * k + n % 7)
+    cx = rng.standard_normal((8, k)) * 2.0
+    x = cx[rng.integers(0, 8, n)] + rng.standard_normal((n, k)) * 0.7
+    rot = np.linalg.qr(rng.standard_normal((k, k)))[0]
+    z = cx[rng.integers(0, 8, m)] @ rot + rng.standard_normal((m, k)) * 0.7
+    a, b = np.full(n, 1 / n), np.full(m, 1 / m)
+    g = rng.standard_normal(m) * 3.0 + (z * z).sum(1)
+    eps = 1.25e-3
+    want = O.softmin(O.SqEuclid(x, z), np.log(b), g, eps)
+    got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, 3)
+    plain = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, 0)
+    lam = np.log2(np.e) / eps  # per-row errors in log2 units of the plan entries
+    e_c, e_p = np.abs(got - want) * lam, np.abs(plain - want) * lam
+    print(f"k={k} n={n} m={m}: rel f32c {_rel(got, want):.2e} f32 {_rel(plain, want):.2e}; "
+          f"p99 log2 err f32c {np.percentile(e_c, 99):.2e} f32 {np.percentile(e_p, 99):.2e}")
+    assert _rel(got, want) < 1e-5
+    assert np.percentile(e_c, 99) < 0.5 * np.percentile(e_p, 99)
+
+
+@pytest.mark.parametrize("limit", ["0", "2000"])
+def test_centred_path_fp64_tile_fallback(env, limit, monkeypatch):
+    """Tile pairs whose fp32 pair-term bound exceeds CNTGW_CTR_TILE_LIMIT are
+    taken in fp64 inside the kernel: with limit 0 every pair is (fp64-exact,
+    the fp64 path's tolerance), with a mid limit the two kinds mix."""
+    P, engine, S, O, torch, dev = env
+    rng = np.random.default_rng(3)
+    n, m, k = 3000, 2600, 3
+    x = rng.standard_normal((n, k)) * 2.5
+    z = rng.standard_normal((m, k)) * 2.5
+    a, b = np.full(n, 1 / n), np.full(m, 1 / m)
+    g = rng.standard_normal(m) * 3.0 + (z * z).sum(1)
+    eps = 1.25e-3
+    want = O.softmin(O.SqEuclid(x, z), np.log(b), g, eps)
+    monkeypatch.setenv("CNTGW_CTR_TILE_LIMIT", limit)
+    got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, 3)
+    assert _rel(got, want) < (5e-7 if limit == "0" else 1e-5)
 
 
 @pytest.mark.parametrize("k", [1, 3, 4, 8, 16, 33, 64])
