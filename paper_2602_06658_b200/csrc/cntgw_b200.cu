@@ -9,6 +9,7 @@
 #include "common.cuh"
 #include "softmin.cuh"
 #include "softmin_ctr.cuh"
+#include "softmin_ctr_tc.cuh"
 #include "softmin_dmma.cuh"
 #include "softmin_tc.cuh"
 #include "sweep.cuh"
@@ -190,10 +191,22 @@ KernelPick pick_ctr() {
   return k;
 }
 
+// CNTGW_F32C, kx <= 4, on tcgen05 (softmin_ctr_tc.cuh); CNTGW_CTR_TC=0 keeps FFMA2
+KernelPick pick_ctc() {
+  KernelPick k;
+  k.fn = (void*)softmin_ctc_kernel<16>;
+  k.rows = 1;  // one 128-row group per CTA
+  k.smem = CtcSmem<16>::kBytes;
+  k.threads = ctc_threads(16);
+  k.rec_bytes = 16 * sizeof(float) + (kCtcKx + 1) * sizeof(double);
+  return k;
+}
+
 bool lookup(int prec, int kd, int sq, KernelPick* out) {
   if (prec == CNTGW_F32C) {
     if (!kd_supported(kd)) return false;
     const int kx = kd + (sq ? 1 : 0);
+    if (kx <= 4 && env_int("CNTGW_CTR_TC", 1)) { *out = pick_ctc(); return true; }
     if (kx <= 4) { *out = pick_ctr<4>(); return true; }
     if (kx <= 8) { *out = pick_ctr<8>(); return true; }
     return false;
@@ -516,7 +529,7 @@ size_t cntgw_ctr_rows_bytes(int64_t n, int kd, int sq_flag) {
 
 size_t cntgw_ctr_cols_bytes(int64_t m, int kd, int sq_flag) {
   const int kx = ctr_kx(kd, sq_flag);
-  return (kx < 0 || m < 1) ? 0 : ctr_cols_bytes(cntgw_cols_padded(m), kx);
+  return (kx < 0 || m < 1) ? 0 : ctr_cols_bytes_all(cntgw_cols_padded(m), kx);
 }
 
 int cntgw_prep_rows_ctr(int kd, int sq_flag, const double* feat, int64_t ld, const double* sq,
@@ -546,9 +559,12 @@ int cntgw_prep_cols_ctr(const cntgw_sweep_state* st, int kd, int sq_flag, const 
   const unsigned tiles = (unsigned)(mpad / kColTile);
   cudaStream_t s = as_stream(stream);
   const int sqf = sq_flag ? 1 : 0;
-  if (kx == 4)
+  if (kx == 4) {
     prep_cols_ctr_kernel<4><<<tiles, kColTile, 0, s>>>(st, kd, sqf, feat, ld, sq, pot, log2w, order, m, mpad, cols);
-  else
+    const CtrCols cv = ctr_cols_view(cols, mpad, 4);
+    prep_cols_ctc_kernel<<<(unsigned)(mpad / 256), 256, 0, s>>>(
+        cv.rec32, mpad, reinterpret_cast<float*>(static_cast<char*>(cols) + ctr_cols_bytes(mpad, 4)));
+  } else
     prep_cols_ctr_kernel<8><<<tiles, kColTile, 0, s>>>(st, kd, sqf, feat, ld, sq, pot, log2w, order, m, mpad, cols);
   return check_launch("prep_cols_ctr");
 }

@@ -70,6 +70,14 @@ __device__ __forceinline__ double f32_to_f64_alu(float v) {
   return __hiloint2double((int)hi, (int)(hi ? u << 29 : 0u));
 }
 
+// Signed variant of f32_to_f64_alu (normal v of either sign exact; 0 and
+// subnormals -> +-0).
+__device__ __forceinline__ double f32_to_f64_alu_s(float v) {
+  const uint32_t u = __float_as_uint(v), mag = u & 0x7fffffffu;
+  const uint32_t hi = mag >= 0x00800000u ? (mag >> 3) + (896u << 20) : 0u;
+  return __hiloint2double((int)(hi | (u & 0x80000000u)), (int)(hi ? mag << 29 : 0u));
+}
+
 // Float-float running sum (hi + lo, ~44-bit significand) on the FMA pipe: the
 // epilogue of the tcgen05 kernel folds one fp32 tile sum per row per tile, and
 // a DADD there stalls on math-pipe throttle behind the MUFU.EX2 stream.

@@ -55,6 +55,10 @@ __host__ __device__ inline size_t ctr_cols_bytes(int64_t mpad, int kx) {
   return align256(sizeof(double) * mpad * (kx + 1)) + align256(sizeof(float) * mpad * kx) +
          align256(sizeof(double) * (mpad / kColTile) * (kx + 1));
 }
+// + the tcgen05 B' tiles of the kx = 4 block (softmin_ctr_tc.cuh): 16 floats per column
+__host__ __device__ inline size_t ctr_cols_bytes_all(int64_t mpad, int kx) {
+  return ctr_cols_bytes(mpad, kx) + (kx == 4 ? sizeof(float) * 16 * (size_t)mpad : 0);
+}
 __host__ __device__ inline size_t ctr_rows_bytes(int64_t n, int kx) {
   const int64_t np = ctr_groups(n) * kCtrRowGroup;
   return align256(sizeof(int64_t) * n) + align256(sizeof(double) * ctr_groups(n) * (kx + 1)) +

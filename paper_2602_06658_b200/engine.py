@@ -298,6 +298,17 @@ class HalfUpdate:
         wsb = max(LIB.cntgw_softmin_workspace(p, rows.n, cols.n, self.kd, int(self.sq)) for p in precs)
         self.ws = torch.empty(max(int(wsb), 16), dtype=torch.uint8, device=dev)
 
+    @property
+    def prec(self) -> int:
+        return self._prec
+
+    @prec.setter
+    def prec(self, p: int):
+        if p == F32C:  # locality orders are computed eagerly, never inside a graph capture
+            self.rows.locality()
+            self.cols.locality()
+        self._prec = p
+
     def pack(self, state: SweepState, pot_cols: torch.Tensor | None, prec=None):
         prec = self.prec if prec is None else prec
         c = self.cols

@@ -50,11 +50,23 @@ def _half_update(env, cost, a, b, g, eps, prec=None):
     return out.cpu().numpy() + prob.row_sep
 
 
-@pytest.mark.parametrize("prec", [0, 1, 3], ids=["f32", "f64", "f32c"])
+# "f32c" runs the centred path's tcgen05 kernel where kd + sq <= 4 (its FFMA2
+# kernel above); "f32c_ffma" forces the FFMA2 kernel (CNTGW_CTR_TC=0)
+PRECS = {"f32": 0, "f64": 1, "f32c": 3, "f32c_ffma": 3}
+
+
+def _prec(name, monkeypatch):
+    if name == "f32c_ffma":
+        monkeypatch.setenv("CNTGW_CTR_TC", "0")
+    return PRECS[name]
+
+
+@pytest.mark.parametrize("pname", list(PRECS))
 @pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 8, 16, 17, 33, 64, 65])
 @pytest.mark.parametrize("n,m", [(1, 1), (1, 300), (300, 1), (129, 257), (1000, 1000), (2049, 771)])
-def test_sq_euclidean_half_update(env, k, n, m, prec):
+def test_sq_euclidean_half_update(env, k, n, m, pname, monkeypatch):
     P, engine, S, O, torch, dev = env
+    prec = _prec(pname, monkeypatch)
     if prec == 3 and not engine.ctr_supported(engine.padded_kd(max(k - 1, 1)), True):
         pytest.skip("centred fp32 path: kd + sq <= 8")
     rng = np.random.default_rng(k * 1000 + n + m)
@@ -84,10 +96,11 @@ def test_low_rank_half_update(env, k):
     assert _rel(got, want) < 1e-5
 
 
-@pytest.mark.parametrize("prec", [0, 1, 3], ids=["f32", "f64", "f32c"])
-def test_rebase_path_under_huge_exponents(env, prec):
+@pytest.mark.parametrize("pname", list(PRECS))
+def test_rebase_path_under_huge_exponents(env, pname, monkeypatch):
     """Cold regime: |exponent| ~ 1e6 log2 units; exercises lazy rebasing."""
     P, engine, S, O, torch, dev = env
+    prec = _prec(pname, monkeypatch)
     rng = np.random.default_rng(0)
     x = rng.standard_normal((700, 4)) * 6.0
     z = rng.standard_normal((900, 4)) * 6.0
@@ -99,14 +112,16 @@ def test_rebase_path_under_huge_exponents(env, prec):
     assert _rel(got, want) < (5e-7 if prec == 1 else 1e-5)
 
 
+@pytest.mark.parametrize("tc", ["1", "0"], ids=["tcgen05", "ffma"])
 @pytest.mark.parametrize("k", [1, 2, 3, 4])
 @pytest.mark.parametrize("n,m", [(5000, 7000), (130, 100_000)])
-def test_centred_path_cold_locality(env, k, n, m):
+def test_centred_path_cold_locality(env, k, n, m, tc, monkeypatch):
     """CNTGW_F32C on a cold clustered law (|exponent| ~ 1e5-1e6 log2 units,
     where plain fp32 loses ~0.1 log2 units per term): fp32 pair terms on
     Morton-ordered centred tiles match the fp64 oracle; outputs come back in
     the caller's (unsorted) order."""
     P, engine, S, O, torch, dev = env
+    monkeypatch.setenv("CNTGW_CTR_TC", tc)
     rng = np.random.default_rng(10 * k + n % 7)
     cx = rng.standard_normal((8, k)) * 2.0
     x = cx[rng.integers(0, 8, n)] + rng.standard_normal((n, k)) * 0.7
@@ -126,8 +141,9 @@ def test_centred_path_cold_locality(env, k, n, m):
     assert np.percentile(e_c, 99) < 0.5 * np.percentile(e_p, 99)
 
 
+@pytest.mark.parametrize("tc", ["1", "0"], ids=["tcgen05", "ffma"])
 @pytest.mark.parametrize("limit", ["0", "2000"])
-def test_centred_path_fp64_tile_fallback(env, limit, monkeypatch):
+def test_centred_path_fp64_tile_fallback(env, limit, tc, monkeypatch):
     """Tile pairs whose fp32 pair-term bound exceeds CNTGW_CTR_TILE_LIMIT are
     taken in fp64 inside the kernel: with limit 0 every pair is (fp64-exact,
     the fp64 path's tolerance), with a mid limit the two kinds mix."""
@@ -140,6 +156,7 @@ def test_centred_path_fp64_tile_fallback(env, limit, monkeypatch):
     g = rng.standard_normal(m) * 3.0 + (z * z).sum(1)
     eps = 1.25e-3
     want = O.softmin(O.SqEuclid(x, z), np.log(b), g, eps)
+    monkeypatch.setenv("CNTGW_CTR_TC", tc)
     monkeypatch.setenv("CNTGW_CTR_TILE_LIMIT", limit)
     got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, 3)
     assert _rel(got, want) < (5e-7 if limit == "0" else 1e-5)

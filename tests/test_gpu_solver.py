@@ -143,6 +143,36 @@ def test_law_trajectory(P, name, eps, n_inner):
             P.solve_cnt_gw(src, tgt, cfg)
 
 
+@pytest.mark.parametrize("name,eps,n_inner", [("c4law_solve", 0.01, 100), ("c5law_solve", 0.02, 200)])
+def test_law_trajectory_centred_path(P, name, eps, n_inner, monkeypatch):
+    """The same reduced-N reference trajectories through the CNTGW_F32C
+    half-updates (forced; at these sizes most tile pairs take the kernel's
+    fp64 fallback, the rest the centred fp32 sweep)."""
+    from paper_2602_06658_b200 import solvers
+
+    monkeypatch.setenv("CNTGW_PRECISION", "f32c")
+    gold = golden(name)
+    src, tgt = _measures(P, gold)
+    state = solvers._CntGwState(src, tgt, P.make_config(eps, n_inner=n_inner, max_outer=10))
+    objs = []
+    for k in range(10):
+        objs.append(state.step().objective)
+        assert _rel(state.coupling().f, gold["f_steps"][k]) < TOL, f"step {k + 1}: f"
+        assert _rel(state.coupling().g, gold["g_steps"][k]) < TOL, f"step {k + 1}: g"
+    assert _rel(objs, gold["objective"]) < TOL
+
+
+def test_device_graph_loop_centred_path(P, monkeypatch):
+    """Whole-solve CUDA graph with the centred path forced: the C1 reference
+    solve (stop step, inner counts, value)."""
+    monkeypatch.setenv("CNTGW_PRECISION", "f32c")
+    gold = golden("c1_solve")
+    src, tgt = _measures(P, gold)
+    res = P.solve_cnt_gw(src, tgt, P.make_config(0.01, threshold=1e-5, max_inner=200, max_outer=20))
+    assert list(res.trace.inner_iters) == [int(v) for v in gold["inner_iters"]]
+    assert _rel([res.value], [float(gold["value"])]) < TOL
+
+
 def test_device_graph_loop_equals_host_loop(P, monkeypatch):
     """The single-graph solve (nested conditional WHILE nodes) and the
     host-driven loop run the same kernels: identical trajectories."""

@@ -59,23 +59,16 @@ def half_update_error(which, n, warm_sweeps):
     state = dev.loop.state
     state.init(eps / 8)
     out = {}
+    variants = (("f64", F64, "1"), ("f32c", F32C, "1"), ("f32c_ffma", F32C, "0"), ("f32", F32, "1"))
     for name, op, pot, length in (("f", dev.fwd, st.g, dev.n), ("g", dev.bwd, st.f, dev.m)):
-        res = {}
-        for prec in (F64, F32C, F32):
+        res, d = {}, {}
+        for tag, prec, tc in variants:
+            os.environ["CNTGW_CTR_TC"] = tc
             op.prec = prec
             o = torch.empty(length, dtype=torch.float64, device=dev.device)
             op(state, pot, o, skip=False)
-            res[prec] = o
-        d = {}
-        for prec, tag in ((F32C, "f32c"), (F32, "f32")):
-            e = ((res[prec] - res[F64]).abs() * lam).cpu().numpy()
-            d[tag] = dict(max=float(e.max()), p99=float(np.percentile(e, 99)), median=float(np.median(e)),
-                          rel=rel(res[prec].cpu().numpy(), res[F64].cpu().numpy()))
-        # device time per launch of each path (CUDA events, 3 launches after a warm-up)
-        for prec, tag in ((F64, "f64"), (F32C, "f32c"), (F32, "f32")):
-            op.prec = prec
-            o = torch.empty(length, dtype=torch.float64, device=dev.device)
-            op(state, pot, o, skip=False)
+            res[tag] = o.clone()
+            # device time per launch (CUDA events, 3 launches after the one above)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(3):
@@ -83,6 +76,11 @@ def half_update_error(which, n, warm_sweeps):
             e1.record()
             torch.cuda.synchronize()
             d[tag + "_pairs_per_s"] = 3.0 * dev.n * dev.m / (e0.elapsed_time(e1) * 1e-3)
+        os.environ["CNTGW_CTR_TC"] = "1"
+        for tag, _, _ in variants[1:]:
+            e = ((res[tag] - res["f64"]).abs() * lam).cpu().numpy()
+            d[tag] = dict(max=float(e.max()), p99=float(np.percentile(e, 99)), median=float(np.median(e)),
+                          rel=rel(res[tag].cpu().numpy(), res["f64"].cpu().numpy()))
         out[name] = d
     out["centred_scale"] = engine.centred_scale(eps / 8, dev.src, dev.tgt)
     out["deferred_fraction"] = [engine.centred_deferred_fraction(eps / 8, dev.src, dev.tgt),
