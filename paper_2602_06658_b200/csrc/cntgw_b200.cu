@@ -194,7 +194,14 @@ KernelPick pick_ctr() {
 // CNTGW_F32C, kx <= 4, on tcgen05 (softmin_ctr_tc.cuh); CNTGW_CTR_TC=0 keeps FFMA2
 KernelPick pick_ctc() {
   KernelPick k;
-  k.fn = (void*)softmin_ctc_kernel<16>;
+  // CNTGW_CTR_TC_POLY: pairs (of 16 per 32-column chunk) exponentiated on the FMA pipe
+  switch (env_int("CNTGW_CTR_TC_POLY", 4)) {
+    case 0: k.fn = (void*)softmin_ctc_kernel<16, 0>; break;
+    case 2: k.fn = (void*)softmin_ctc_kernel<16, 2>; break;
+    case 6: k.fn = (void*)softmin_ctc_kernel<16, 6>; break;
+    case 8: k.fn = (void*)softmin_ctc_kernel<16, 8>; break;
+    default: k.fn = (void*)softmin_ctc_kernel<16, 4>; break;
+  }
   k.rows = 1;  // one 128-row group per CTA
   k.smem = CtcSmem<16>::kBytes;
   k.threads = ctc_threads(16);

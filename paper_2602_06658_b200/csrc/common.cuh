@@ -43,6 +43,13 @@ __device__ __forceinline__ float f64_to_f32_alu(double v) {
   return __uint_as_float((f & 0x7fffffffu) | (hi & 0x80000000u));
 }
 
+// double -> float rounded to nearest on the ALU (|v| < 2^127): add half an
+// fp32 ulp to the 29 mantissa bits the truncation drops, then truncate.
+__device__ __forceinline__ float f64_to_f32_rn_alu(double v) {
+  const long long w = __double_as_longlong(v) + (1LL << 28);
+  return f64_to_f32_alu(__longlong_as_double(w));
+}
+
 // Cheaper conversion for the streaming fp64 softmin (3 ALU ops: IADD, SHF,
 // LOP3): the kernel keeps every exponent argument away from zero by carrying
 // its row reference kRefOffset log2 units above the row minimum, so the only

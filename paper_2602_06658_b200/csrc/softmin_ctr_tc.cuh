@@ -73,7 +73,7 @@ struct CtcSmem {
   static constexpr size_t kBytes = kA + kB + kR + kF;
 };
 
-template <int EPI>
+template <int EPI, int NPOLY>
 __global__ void __launch_bounds__(ctc_threads(EPI), 1) softmin_ctc_kernel(const SoftminArgs a) {
   using SM = CtcSmem<EPI>;
   extern __shared__ __align__(1024) unsigned char smem_ctc[];
@@ -204,7 +204,11 @@ __global__ void __launch_bounds__(ctc_threads(EPI), 1) softmin_ctc_kernel(const 
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int col = lane + 32 * u;
-        const float v = -(float)(A[u] - mn);  // -bias; padding columns -> -1e30 (zero weight)
+        // -bias as two tf32 terms of its fp32 rounding; the double -> float
+        // conversion on the ALU (F2F would queue on the XU pipe behind the
+        // epilogue's MUFU stream and stall this warp, the MMA's critical path);
+        // padding columns -> -1e30 (zero weight)
+        const float v = f64_to_f32_rn_alu(mn - A[u]);
         const float vh = tf32_rna(v);
         bt[(CtcL::kHi + kCtcKx) / 4 * (kTcCols * 4) + col * 4 + (CtcL::kHi + kCtcKx) % 4] = vh;
         bt[(CtcL::kLo + kCtcKx) / 4 * (kTcCols * 4) + col * 4 + (CtcL::kLo + kCtcKx) % 4] =
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(ctc_threads(EPI), 1) softmin_ctc_kernel(const 
         if (lane == 0) mbar_arrive(&tempty_bar[ab]);
         continue;
       }
-      float mref = f64_to_f32_alu(M - off);  // (sign-correct for |.| >= 2^-126)
+      float mref = f64_to_f32_rn_alu(M - off);  // (no F2F on the XU pipe)
       if (!(M - off > -1e30)) mref = -CUDART_INF_F;
       const float mref0 = mref;
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) +
@@ -303,7 +307,7 @@ __global__ void __launch_bounds__(ctc_threads(EPI), 1) softmin_ctc_kernel(const 
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty_bar[ab]);
         }
-        tc_chunk<0>(cur, mref, tsum, S);
+        tc_chunk<NPOLY>(cur, mref, tsum, S);
         if (c + 1 < kChunksPerPart) tmem_wait_ld();
       }
       S.add(tsum);

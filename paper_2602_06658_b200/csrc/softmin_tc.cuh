@@ -155,6 +155,7 @@ __device__ __forceinline__ void tc_chunk(const float (&v)[32], float& mref, floa
     constexpr uint32_t kMask = NPOLY == 2   ? 0x0201u
                                : NPOLY == 4 ? 0x8421u
                                : NPOLY == 6 ? 0x9249u
+                               : NPOLY == 8 ? 0x5555u
                                             : 0u;
     const bool poly = (kMask >> u) & 1u;
     acc[u & 3] = add2(acc[u & 3], poly ? exp2_poly2(x) : f2(ex2(x.x), ex2(x.y)));
