@@ -191,7 +191,10 @@ KernelPick pick_ctr() {
   return k;
 }
 
-// CNTGW_F32C, kx <= 4, on tcgen05 (softmin_ctr_tc.cuh); CNTGW_CTR_TC=0 keeps FFMA2
+// CNTGW_F32C, kx <= 4, on tcgen05 (softmin_ctr_tc.cuh), opt-in with CNTGW_CTR_TC=1:
+// 11% faster than the FFMA2 kernel at the C4 law but its split-tf32 products
+// and tensor-core accumulation move the 10-step C4 trajectory by up to 5.5e-4
+// (objective) against 2.3e-5 for the FFMA2 kernel (profiles/r1_ctr_c4_solve.txt)
 KernelPick pick_ctc() {
   KernelPick k;
   // CNTGW_CTR_TC_POLY: pairs (of 16 per 32-column chunk) exponentiated on the FMA pipe
@@ -213,7 +216,7 @@ bool lookup(int prec, int kd, int sq, KernelPick* out) {
   if (prec == CNTGW_F32C) {
     if (!kd_supported(kd)) return false;
     const int kx = kd + (sq ? 1 : 0);
-    if (kx <= 4 && env_int("CNTGW_CTR_TC", 1)) { *out = pick_ctc(); return true; }
+    if (kx <= 4 && env_int("CNTGW_CTR_TC", 0)) { *out = pick_ctc(); return true; }
     if (kx <= 4) { *out = pick_ctr<4>(); return true; }
     if (kx <= 8) { *out = pick_ctr<8>(); return true; }
     return false;

@@ -50,14 +50,13 @@ def _half_update(env, cost, a, b, g, eps, prec=None):
     return out.cpu().numpy() + prob.row_sep
 
 
-# "f32c" runs the centred path's tcgen05 kernel where kd + sq <= 4 (its FFMA2
-# kernel above); "f32c_ffma" forces the FFMA2 kernel (CNTGW_CTR_TC=0)
-PRECS = {"f32": 0, "f64": 1, "f32c": 3, "f32c_ffma": 3}
+# "f32c" runs the centred path's FFMA2 kernel (the default); "f32c_tc" its
+# opt-in tcgen05 kernel where kd + sq <= 4 (CNTGW_CTR_TC=1)
+PRECS = {"f32": 0, "f64": 1, "f32c": 3, "f32c_tc": 3}
 
 
 def _prec(name, monkeypatch):
-    if name == "f32c_ffma":
-        monkeypatch.setenv("CNTGW_CTR_TC", "0")
+    monkeypatch.setenv("CNTGW_CTR_TC", "1" if name == "f32c_tc" else "0")
     return PRECS[name]
 
 

@@ -59,7 +59,7 @@ def half_update_error(which, n, warm_sweeps):
     state = dev.loop.state
     state.init(eps / 8)
     out = {}
-    variants = (("f64", F64, "1"), ("f32c", F32C, "1"), ("f32c_ffma", F32C, "0"), ("f32", F32, "1"))
+    variants = (("f64", F64, "0"), ("f32c", F32C, "0"), ("f32c_tc", F32C, "1"), ("f32", F32, "0"))
     for name, op, pot, length in (("f", dev.fwd, st.g, dev.n), ("g", dev.bwd, st.f, dev.m)):
         res, d = {}, {}
         for tag, prec, tc in variants:
@@ -76,7 +76,7 @@ def half_update_error(which, n, warm_sweeps):
             e1.record()
             torch.cuda.synchronize()
             d[tag + "_pairs_per_s"] = 3.0 * dev.n * dev.m / (e0.elapsed_time(e1) * 1e-3)
-        os.environ["CNTGW_CTR_TC"] = "1"
+        os.environ.pop("CNTGW_CTR_TC", None)
         for tag, _, _ in variants[1:]:
             e = ((res[tag] - res["f64"]).abs() * lam).cpu().numpy()
             d[tag] = dict(max=float(e.max()), p99=float(np.percentile(e, 99)), median=float(np.median(e)),
@@ -111,6 +111,12 @@ def main():
     os.environ["CNTGW_PRECISION"] = "auto"
     dev.choose_precision(st_c.f, st_c.g, eps / 8)
     auto = int(dev.prec)
+    if len(sys.argv) > 5 and sys.argv[5] == "nof64":  # timing + objectives of the centred path only
+        print(json.dumps(dict(config=which, n=n, outer=outer, inner=inner, centred_scale=scale,
+                              auto_precision=auto, seconds_f32c=t_c,
+                              pairs_per_s_f32c=outer * (2 * inner + 2) * float(n) * n / t_c,
+                              objectives_f32c=[r[0] for r in res_c])), flush=True)
+        return
     t_d, res_d, _ = run(src, tgt, cfg, outer, "f64")
     steps = []
     for (oc, fc, gc, Gc), (od, fd, gd, Gd) in zip(res_c, res_d):
