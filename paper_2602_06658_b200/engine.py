@@ -106,6 +106,10 @@ def exponent_scale(eps: float, feat_r, sq_r, feat_c, sq_c, pot_abs: float = 0.0)
 # CTR_MAX_DEFERRED of the pairs need that fallback (softmin_ctr.cuh).
 CTR_TILE_LIMIT = float(os.environ.get("CNTGW_CTR_TILE_LIMIT", 65536.0))
 CTR_MAX_DEFERRED = 0.05
+# ... and only for half-updates of at least this many pairs: below it the
+# fp64 kernels take well under a millisecond and keep fp64-level agreement
+# with the reference's discrete decisions (threshold stops, divergence guard)
+CTR_MIN_PAIRS = float(os.environ.get("CNTGW_CTR_MIN_PAIRS", 2.0 ** 28))
 CTR_ROW_GROUP, CTR_COL_TILE = 128, 256
 
 
@@ -159,6 +163,14 @@ def centred_scale(eps: float, rows: "Side", cols: "Side") -> float:
     """Worst (group, tile) bound of the fp32 pair term (diagnostic)."""
     rr, rc = centred_radii(eps, rows, cols)
     return float(rr.max() * rc.max())
+
+
+def centred_choice_fraction(eps: float, rows: "Side", cols: "Side") -> float:
+    """The deferred fraction choose_precision compares (both half-update
+    directions), or 1.0 for problems below CTR_MIN_PAIRS."""
+    if float(rows.n) * float(cols.n) < CTR_MIN_PAIRS:
+        return 1.0
+    return max(centred_deferred_fraction(eps, rows, cols), centred_deferred_fraction(eps, cols, rows))
 
 
 def centred_deferred_fraction(eps: float, rows: "Side", cols: "Side") -> float:

@@ -245,9 +245,8 @@ def _set_precision(problem, eps, f0, g0):
     scale = engine.exponent_scale(eps, fwd.rows.feat64, fwd.rows.sq64, fwd.cols.feat64,
                                   fwd.cols.sq64, pot)
     prec = engine.choose_precision(scale, fwd.kd, fwd.sq,
-                                   ctr_deferred=lambda: max(
-                                       engine.centred_deferred_fraction(eps, fwd.rows, fwd.cols),
-                                       engine.centred_deferred_fraction(eps, fwd.cols, fwd.rows)))
+                                   ctr_deferred=lambda: engine.centred_choice_fraction(
+                                       eps, fwd.rows, fwd.cols))
     problem.fwd.prec = prec
     problem.bwd.prec = prec
 

@@ -300,6 +300,8 @@ class _GwDevice:
         self.loop.set_precision(self.prec)
 
     def _ctr_deferred(self, eps_min):
+        if float(self.n_total) * float(self.m) < engine.CTR_MIN_PAIRS:
+            return 1.0
         s = max(engine.centred_deferred_fraction(eps_min, self.src, self.tgt),
                 engine.centred_deferred_fraction(eps_min, self.tgt, self.src))
         if self.comm is not None:  # every rank must pick the same path
