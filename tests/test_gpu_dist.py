@@ -22,9 +22,11 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, results):
+def _worker(rank, world, port, results, precision="auto"):
     import torch
     import torch.distributed as dist
+
+    os.environ["CNTGW_PRECISION"] = precision
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK="0")
@@ -43,11 +45,15 @@ def _worker(rank, world, port, results):
     dist.destroy_process_group()
 
 
-def test_two_rank_sharded_solve_matches_reference():
+@pytest.mark.parametrize("precision", ["auto", "f32c"])
+def test_two_rank_sharded_solve_matches_reference(precision):
+    """auto: the fp64/fp32 kernels the problem selects; f32c: the centred
+    kernel forced, whose per-shard locality orders and scattered partial-LSE
+    outputs must combine like the unsharded ones."""
     world = 2
     mgr = mp.Manager()
     results = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), results, precision), nprocs=world, join=True)
     g = golden("c1_solve")
     v0, f0, g0, it0, gam0, am0 = results[0]
     v1, f1, g1, it1, gam1, am1 = results[1]
