@@ -437,12 +437,18 @@ __global__ void __launch_bounds__(128, MINB) softmin_ctr_kernel(const SoftminArg
     for (int r = 0; r < R; ++r) bad |= (grad[r] * radJ > a.ctr_limit ? 1u : 0u) << r;
     double rho[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) rho[r] = fmin(fmin(red[0][r], red[1][r]), fmin(red[2][r], red[3][r]));
+    for (int r = 0; r < R; ++r) {
+      rho[r] = fmin(fmin(red[0][r], red[1][r]), fmin(red[2][r], red[3][r]));
+      if (!(rho[r] < CUDART_INF)) rho[r] = 0.0;  // a tile of zero-weight columns: all biases +inf
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       float bb[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) bb[r] = (bad >> r) & 1u ? CUDART_INF_F : (float)(A[r][h] - rho[r]);
+      // (finite cap: a zero-weight column, A = +inf, must not meet an infinite
+      // row reference as inf - inf)
+      for (int r = 0; r < R; ++r)
+        bb[r] = (bad >> r) & 1u ? CUDART_INF_F : (float)fmin(A[r][h] - rho[r], kPadQ);
       float4* b4 = reinterpret_cast<float4*>(sbias + (tid + 128 * h) * R);
 #pragma unroll
       for (int v = 0; v < R / 4; ++v) b4[v] = make_float4(bb[4 * v], bb[4 * v + 1], bb[4 * v + 2], bb[4 * v + 3]);
@@ -495,7 +501,7 @@ __global__ void __launch_bounds__(128, MINB) softmin_ctr_kernel(const SoftminArg
             double acc = rj[KX];
 #pragma unroll
             for (int k = 0; k < KX; ++k) acc = fma(xi[k], rj[k], acc);
-            qv[u] = acc;
+            qv[u] = fmin(acc, kPadQ);  // zero-weight columns: finite, zero-weight terms
           }
           double qmin = qv[0];
 #pragma unroll

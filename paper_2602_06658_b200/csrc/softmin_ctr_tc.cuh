@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(ctc_threads(EPI), 1) softmin_ctc_kernel(const 
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      if (!(mn < CUDART_INF)) mn = 0.0;  // a tile of zero-weight columns: all biases +inf
       const double radJ = cols.tctr[J * (kCtcKx + 1) + kCtcKx];
       const bool bad = grad * radJ > a.ctr_limit;
       float* bt = sB + s * CtcL::kBTileFloats;
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(ctc_threads(EPI), 1) softmin_ctc_kernel(const 
         // conversion on the ALU (F2F would queue on the XU pipe behind the
         // epilogue's MUFU stream and stall this warp, the MMA's critical path);
         // padding columns -> -1e30 (zero weight)
-        const float v = f64_to_f32_rn_alu(mn - A[u]);
+        const float v = f64_to_f32_rn_alu(fmax(mn - A[u], -kPadQ));  // (zero weights: A = +inf)
         const float vh = tf32_rna(v);
         bt[(CtcL::kHi + kCtcKx) / 4 * (kTcCols * 4) + col * 4 + (CtcL::kHi + kCtcKx) % 4] = vh;
         bt[(CtcL::kLo + kCtcKx) / 4 * (kTcCols * 4) + col * 4 + (CtcL::kLo + kCtcKx) % 4] =
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(ctc_threads(EPI), 1) softmin_ctc_kernel(const 
             double acc = rj[kCtcKx];
 #pragma unroll
             for (int k = 0; k < kCtcKx; ++k) acc = fma(xi[k], rj[k], acc);
-            tv[u] = -acc;
+            tv[u] = fmax(-acc, -kPadQ);
           }
           double tmax = tv[0];
 #pragma unroll

@@ -142,6 +142,29 @@ def test_centred_path_cold_locality(env, k, n, m, tc, monkeypatch):
 
 
 @pytest.mark.parametrize("tc", ["1", "0"], ids=["tcgen05", "ffma"])
+def test_centred_path_zero_weight_region(env, tc, monkeypatch):
+    """Zero column weights (the reference's sinkhorn accepts them: log 0 =
+    -inf terms) on a whole spatial region, so that entire Morton tiles carry
+    no mass: the centred kernels must give those tiles zero weight, not NaN."""
+    P, engine, S, O, torch, dev = env
+    monkeypatch.setenv("CNTGW_CTR_TC", tc)
+    rng = np.random.default_rng(5)
+    n, m = 2000, 6000
+    x = rng.standard_normal((n, 3)) * 2.0
+    z = rng.standard_normal((m, 3)) * 2.0
+    a = np.full(n, 1 / n)
+    b = np.where(z[:, 0] > 0.5, 0.0, 1.0)
+    b /= b.sum()
+    g = rng.standard_normal(m) + (z * z).sum(1)
+    eps = 2.5e-3
+    with np.errstate(divide="ignore"):
+        want = O.softmin(O.SqEuclid(x, z), np.log(b), g, eps)
+    got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, 3)
+    assert np.all(np.isfinite(got))
+    assert _rel(got, want) < 1e-5
+
+
+@pytest.mark.parametrize("tc", ["1", "0"], ids=["tcgen05", "ffma"])
 @pytest.mark.parametrize("limit", ["0", "2000"])
 def test_centred_path_fp64_tile_fallback(env, limit, tc, monkeypatch):
     """Tile pairs whose fp32 pair-term bound exceeds CNTGW_CTR_TILE_LIMIT are
