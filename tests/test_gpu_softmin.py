@@ -141,13 +141,13 @@ def test_centred_path_cold_locality(env, k, n, m, tc, monkeypatch):
         assert np.percentile(e_c, 99) < 0.75 * np.percentile(e_p, 99)
 
 
-@pytest.mark.parametrize("tc", ["1", "0"], ids=["tcgen05", "ffma"])
-def test_centred_path_zero_weight_region(env, tc, monkeypatch):
+@pytest.mark.parametrize("pname", list(PRECS))
+def test_zero_weight_region(env, pname, monkeypatch):
     """Zero column weights (the reference's sinkhorn accepts them: log 0 =
-    -inf terms) on a whole spatial region, so that entire Morton tiles carry
-    no mass: the centred kernels must give those tiles zero weight, not NaN."""
+    -inf terms) on a whole spatial region, so that entire Morton tiles (and
+    column groups of the other kernels) carry no mass: zero weight, not NaN."""
     P, engine, S, O, torch, dev = env
-    monkeypatch.setenv("CNTGW_CTR_TC", tc)
+    prec = _prec(pname, monkeypatch)
     rng = np.random.default_rng(5)
     n, m = 2000, 6000
     x = rng.standard_normal((n, 3)) * 2.0
@@ -159,7 +159,7 @@ def test_centred_path_zero_weight_region(env, tc, monkeypatch):
     eps = 2.5e-3
     with np.errstate(divide="ignore"):
         want = O.softmin(O.SqEuclid(x, z), np.log(b), g, eps)
-    got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, 3)
+    got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, prec)
     assert np.all(np.isfinite(got))
     assert _rel(got, want) < 1e-5
 
