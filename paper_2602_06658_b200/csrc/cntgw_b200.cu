@@ -95,6 +95,8 @@ struct KernelPick {
   int threads = 128;
   size_t rec_bytes = 0;  // bytes of column records per column (L2 chunking)
   int cta_rows = 0;      // rows per CTA when not 128 * rows
+  int ctr_kx = 0;        // CNTGW_F32C FFMA2 kernel: feature width and groups per CTA
+  int ctr_r = 0;         //   (block-sparse plan, ctr_plan_kernel)
 };
 
 template <int PREC, int KD, int SQ>
@@ -188,7 +190,19 @@ KernelPick pick_ctr() {
   k.rows = R;
   k.smem = CtrSmem<KX, R>::kBytes;
   k.rec_bytes = (KX + 1) * sizeof(double) + KX * sizeof(float);
+  k.ctr_kx = KX;
+  k.ctr_r = R;
   return k;
+}
+
+// Block-sparse plan of the centred FFMA2 kernel: fp32 rho table [CTA][R][tile]
+// and the needed-tile mask [CTA][tile]; CNTGW_CTR_SKIP=0 disables it.
+bool ctr_skip_enabled(const KernelPick& k) { return k.ctr_kx > 0 && env_int("CNTGW_CTR_SKIP", 1) != 0; }
+size_t ctr_plan_bytes(const KernelPick& k, int64_t n, int64_t m) {
+  if (!ctr_skip_enabled(k)) return 0;
+  const int64_t ctas = (ctr_groups(n) + k.ctr_r - 1) / k.ctr_r;
+  const int64_t tl = (m + kColTile - 1) / kColTile;
+  return align256(sizeof(float) * ctas * k.ctr_r * tl) + align256((size_t)(ctas * tl));
 }
 
 // CNTGW_F32C, kx <= 4, on tcgen05 (softmin_ctr_tc.cuh), opt-in with CNTGW_CTR_TC=1:
@@ -249,6 +263,10 @@ Plan plan_softmin(int64_t n, int64_t m, const KernelPick& k) {
   p.row_tiles = (int)((n + rows_per_cta - 1) / rows_per_cta);
   const int64_t tiles = (m + kColTile - 1) / kColTile;
   int occ = 1;
+  // the dynamic shared-memory opt-in must precede the occupancy query, or a
+  // workspace query made before the first launch plans with a different
+  // occupancy (and chunk count) than the launch itself
+  cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, k.threads, k.smem) != cudaSuccess) {
     cudaGetLastError();
     occ = 1;
@@ -582,7 +600,7 @@ int cntgw_prep_cols_ctr(const cntgw_sweep_state* st, int kd, int sq_flag, const 
 size_t cntgw_softmin_workspace(int prec, int64_t n, int64_t m, int kd, int sq_flag) {
   KernelPick k;
   if (n < 1 || m < 1 || !lookup(prec, kd, sq_flag, &k)) return 0;
-  return plan_workspace(plan_softmin(n, m, k), n);
+  return align256(plan_workspace(plan_softmin(n, m, k), n)) + ctr_plan_bytes(k, n, m);
 }
 
 int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int kd, int sq_flag,
@@ -617,14 +635,26 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
     const char* e = getenv("CNTGW_CTR_TILE_LIMIT");
     a.ctr_limit = e ? atof(e) : 65536.0;
   }
+  const size_t part_bytes = align256(plan_workspace(p, n)), plan_bytes = ctr_plan_bytes(k, n, m);
+  if (part_bytes + plan_bytes > 0 && (workspace == nullptr || workspace_bytes < part_bytes + plan_bytes))
+    return fail(CNTGW_ENOSPACE, "softmin workspace %zu < %zu bytes", workspace_bytes, part_bytes + plan_bytes);
   if (p.nchunks > 1) {
-    const size_t need = plan_workspace(p, n);
-    if (workspace == nullptr || workspace_bytes < need)
-      return fail(CNTGW_ENOSPACE, "softmin workspace %zu < %zu bytes", workspace_bytes, need);
     a.part_max = static_cast<double*>(workspace);
     a.part_sum = a.part_max + (size_t)p.nchunks * n;
   }
   cudaStream_t s = as_stream(stream);
+  if (plan_bytes > 0) {  // block-sparse plan of the centred kernel (ctr_plan_kernel)
+    const int64_t ctas = (ctr_groups(n) + k.ctr_r - 1) / k.ctr_r, tl = (m + kColTile - 1) / kColTile;
+    float* rho = reinterpret_cast<float*>(static_cast<char*>(workspace) + part_bytes);
+    uint8_t* need = reinterpret_cast<uint8_t*>(rho) + align256(sizeof(float) * ctas * k.ctr_r * tl);
+    const char* e = getenv("CNTGW_CTR_SKIP_T");
+    const double T = e ? atof(e) : 64.0;
+    if (k.ctr_kx == 4)
+      ctr_plan_kernel<4, 8><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, T);
+    else
+      ctr_plan_kernel<8, 4><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, T);
+    a.ctr_need = need;
+  }
   void* args[] = {&a};
   const cudaError_t e =
       cudaLaunchKernel(k.fn, dim3(p.row_tiles, p.nchunks), dim3(k.threads), args, k.smem, s);

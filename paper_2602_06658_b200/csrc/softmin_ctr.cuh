@@ -389,18 +389,33 @@ __global__ void __launch_bounds__(128, MINB) softmin_ctr_kernel(const SoftminArg
   const uint32_t b64 = SM::kStage64 * sizeof(double), b32 = SM::kStage32 * sizeof(float);
   const double* src64 = cols.rec64 + c0 * (KX + 1);
   const float* src32 = cols.rec32 + c0 * KX;
+  // Block-sparse plan (ctr_plan_kernel): tiles that cannot hold a term within
+  // 2^-T of any of this CTA's rows' maxima are skipped; every thread walks the
+  // same sequence of needed tiles (a uniform scan of a byte mask in L1/L2).
+  const uint8_t* need = a.ctr_need ? a.ctr_need + (int64_t)blockIdx.x * (mpad / kColTile) + c0 / kColTile
+                                   : nullptr;
+  auto next_needed = [&](int t) {
+    if (need)
+      while (t < ntiles && !need[t]) ++t;
+    return t;
+  };
+  auto load_tile = [&](int s, int t) {
+    mbar_expect_tx(&bars[s], b64 + b32);
+    bulk_g2s(s64 + s * SM::kStage64, src64 + (int64_t)t * SM::kStage64, b64, &bars[s]);
+    bulk_g2s(s32 + s * SM::kStage32, src32 + (int64_t)t * SM::kStage32, b32, &bars[s]);
+  };
+  int tq[2];  // needed tiles in the two stages
+  tq[0] = next_needed(0);
+  tq[1] = next_needed(tq[0] + 1);
   TilePipe pipe{bars};
   pipe.init();  // (also publishes gctr and sM)
   if (tid == 0)
-    for (int s = 0; s < 2 && s < ntiles; ++s) {
-      mbar_expect_tx(&bars[s], b64 + b32);
-      bulk_g2s(s64 + s * SM::kStage64, src64 + (int64_t)s * SM::kStage64, b64, &bars[s]);
-      bulk_g2s(s32 + s * SM::kStage32, src32 + (int64_t)s * SM::kStage32, b32, &bars[s]);
-    }
-  for (int t = 0; t < ntiles; ++t) {
-    const int s = t & 1;
-    const int64_t J = c0 / kColTile + t;
-    mbar_wait(&bars[s], (t >> 1) & 1);
+    for (int s = 0; s < 2; ++s)
+      if (tq[s] < ntiles) load_tile(s, tq[s]);
+  for (int k = 0; tq[k & 1] < ntiles; ++k) {
+    const int s = k & 1;
+    const int64_t J = c0 / kColTile + tq[s];
+    mbar_wait(&bars[s], (k >> 1) & 1);
     // (1) group biases A_j^I = c_j + <Xc_I, Zr_j> for this thread's 2 columns, fp64
     const double* rec = s64 + s * SM::kStage64;
     double A[R][2];
@@ -522,11 +537,8 @@ __global__ void __launch_bounds__(128, MINB) softmin_ctr_kernel(const SoftminArg
       }
     }
     __syncthreads();  // every warp is done with stage s and the biases
-    if (tid == 0 && t + 2 < ntiles) {
-      mbar_expect_tx(&bars[s], b64 + b32);
-      bulk_g2s(s64 + s * SM::kStage64, src64 + (int64_t)(t + 2) * SM::kStage64, b64, &bars[s]);
-      bulk_g2s(s32 + s * SM::kStage32, src32 + (int64_t)(t + 2) * SM::kStage32, b32, &bars[s]);
-    }
+    tq[s] = next_needed(tq[s ^ 1] + 1);  // the needed tile after the one in the other stage
+    if (tid == 0 && tq[s] < ntiles) load_tile(s, tq[s]);
   }
   const double lam = a.st->lam_d, inv_lam = 1.0 / lam;
   const double* rs = static_cast<const double*>(a.row_sq);
@@ -538,6 +550,102 @@ __global__ void __launch_bounds__(128, MINB) softmin_ctr_kernel(const SoftminArg
       const double si = rs ? rs[i] : 0.0;
       softmin_store(a, chunk, i, -sM[r * 128 + tid] - lam * si * si, S[r], inv_lam);
     }
+  }
+}
+
+// ---- block-sparse plan ---------------------------------------------------------
+// For the CTA of R row groups the streaming kernel will use, over ALL column
+// tiles: rho_IJ = min_j A_j^I (fp64, as the streaming prologue), per row
+// B_i^J, and the bounds on the row's terms in tile J (log2 units, t = -q)
+//     t_ij <= -(rho_IJ + B_i^J) + C_IJ,   max_j t_ij >= -(rho_IJ + B_i^J) - C_IJ,
+// C_IJ = R_I R_J the pair-term bound. Pass 1 keeps L_i = max_J of the lower
+// bound and rho (rounded down to fp32: only loosens the upper bound); pass 2
+// marks tile J needed for the CTA when some row has an upper bound above
+// L_i - T. A skipped tile holds only terms below 2^-T of its row's maximum,
+// so with T = 64 the skipped mass is < m 2^-64 of every row's sum.
+template <int KX, int R>
+__global__ void __launch_bounds__(128) ctr_plan_kernel(const SoftminArgs a, float* rho_tab, uint8_t* need,
+                                                       double T) {
+  __shared__ double gctr[R][KX];
+  __shared__ double grad[R];
+  __shared__ double red[4][R];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t mpad = (a.m + kColTile - 1) / kColTile * kColTile;
+  const int64_t TL = mpad / kColTile;
+  const CtrRows rows = ctr_rows_view(a.row_feat, a.n, KX);
+  const CtrCols cols = ctr_cols_view(a.col_rec, mpad, KX);
+  const int64_t g0 = (int64_t)blockIdx.x * R;
+  const int64_t ngroups = ctr_groups(a.n);
+  if (tid < R * KX) {
+    const int r = tid / KX, k = tid % KX;
+    gctr[r][k] = g0 + r < ngroups ? rows.ctr[(g0 + r) * (KX + 1) + k] : 0.0;
+  }
+  if (tid < R) grad[tid] = g0 + tid < ngroups ? rows.ctr[(g0 + tid) * (KX + 1) + KX] : 0.0;
+  __syncthreads();
+  double dx[R][KX];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int k = 0; k < KX; ++k)
+      dx[r][k] = g0 + r < ngroups ? rows.dx64[((g0 + r) * kCtrRowGroup + tid) * KX + k] : 0.0;
+  double L[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) L[r] = -CUDART_INF;
+  float* rho_cta = rho_tab + (int64_t)blockIdx.x * R * TL;
+  for (int64_t J = 0; J < TL; ++J) {  // pass 1
+    double A[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) A[r] = CUDART_INF;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double* rj = cols.rec64 + (J * kColTile + tid + 128 * h) * (KX + 1);
+      double z[KX];
+#pragma unroll
+      for (int k = 0; k < KX; ++k) z[k] = rj[k];
+      const double c = rj[KX];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double acc = c;
+#pragma unroll
+        for (int k = 0; k < KX; ++k) acc = fma(gctr[r][k], z[k], acc);
+        A[r] = fmin(A[r], acc);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double v = A[r];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (lane == 0) red[warp][r] = v;
+    }
+    __syncthreads();
+    const double* tc = cols.tctr + J * (KX + 1);
+    const double radJ = tc[KX];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double rho = fmin(fmin(red[0][r], red[1][r]), fmin(red[2][r], red[3][r]));
+      double b = rho;
+#pragma unroll
+      for (int k = 0; k < KX; ++k) b = fma(dx[r][k], tc[k], b);
+      L[r] = fmax(L[r], -b - grad[r] * radJ);  // (+inf rho: zero-weight tile, no bound)
+      if (tid == 0) rho_cta[r * TL + J] = __double2float_rd(rho);
+    }
+    __syncthreads();  // red[] reuse
+  }
+  __syncthreads();  // rho_cta visible to the block
+  for (int64_t J = 0; J < TL; ++J) {  // pass 2
+    const double* tc = cols.tctr + J * (KX + 1);
+    const double radJ = tc[KX];
+    int keep = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double b = (double)rho_cta[r * TL + J];
+#pragma unroll
+      for (int k = 0; k < KX; ++k) b = fma(dx[r][k], tc[k], b);
+      keep |= (g0 + r < ngroups) && (-b + grad[r] * radJ >= L[r] - T);
+    }
+    keep = __syncthreads_or(keep);
+    if (tid == 0) need[(int64_t)blockIdx.x * TL + J] = (uint8_t)keep;
   }
 }
 

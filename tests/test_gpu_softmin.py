@@ -141,6 +141,31 @@ def test_centred_path_cold_locality(env, k, n, m, tc, monkeypatch):
         assert np.percentile(e_c, 99) < 0.75 * np.percentile(e_p, 99)
 
 
+def test_centred_block_sparse_skip(env, monkeypatch):
+    """The centred kernel's block-sparse plan (tiles that cannot hold a term
+    within 2^-64 of a row's maximum are skipped) on a cold clustered law large
+    enough for most tiles to be skipped: equal to the dense sweep to 1e-9 and
+    to the fp64 oracle on sampled rows."""
+    P, engine, S, O, torch, dev = env
+    rng = np.random.default_rng(11)
+    n = m = 1 << 16
+    cx = rng.standard_normal((8, 3)) * 2.0
+    x = cx[rng.integers(0, 8, n)] + rng.standard_normal((n, 3)) * 0.7
+    z = cx[rng.integers(0, 8, m)] + rng.standard_normal((m, 3)) * 0.7
+    a, b = np.full(n, 1 / n), np.full(m, 1 / m)
+    g = rng.standard_normal(m) * 0.1 + (z * z).sum(1)
+    eps = 1.25e-3
+    cost = P.SquaredEuclideanCost(x, z)
+    monkeypatch.setenv("CNTGW_CTR_SKIP", "1")
+    sparse = _half_update(env, cost, a, b, g, eps, 3)
+    monkeypatch.setenv("CNTGW_CTR_SKIP", "0")
+    dense = _half_update(env, cost, a, b, g, eps, 3)
+    assert _rel(sparse, dense) < 1e-9
+    rows = rng.choice(n, 512, replace=False)
+    want = O.softmin(O.SqEuclid(x, z), np.log(b), g, eps, row_idx=rows)
+    assert _rel(sparse[rows], want) < 1e-5
+
+
 @pytest.mark.parametrize("pname", list(PRECS))
 def test_zero_weight_region(env, pname, monkeypatch):
     """Zero column weights (the reference's sinkhorn accepts them: log 0 =

@@ -59,11 +59,14 @@ def half_update_error(which, n, warm_sweeps):
     state = dev.loop.state
     state.init(eps / 8)
     out = {}
-    variants = (("f64", F64, "0"), ("f32c", F32C, "0"), ("f32c_tc", F32C, "1"), ("f32", F32, "0"))
+    variants = (("f64", F64, {}), ("f32c", F32C, {}), ("f32c_noskip", F32C, {"CNTGW_CTR_SKIP": "0"}),
+                ("f32c_tc", F32C, {"CNTGW_CTR_TC": "1"}), ("f32", F32, {}))
     for name, op, pot, length in (("f", dev.fwd, st.g, dev.n), ("g", dev.bwd, st.f, dev.m)):
         res, d = {}, {}
-        for tag, prec, tc in variants:
-            os.environ["CNTGW_CTR_TC"] = tc
+        for tag, prec, env in variants:
+            for key in ("CNTGW_CTR_TC", "CNTGW_CTR_SKIP"):
+                os.environ.pop(key, None)
+            os.environ.update(env)
             op.prec = prec
             o = torch.empty(length, dtype=torch.float64, device=dev.device)
             op(state, pot, o, skip=False)
@@ -76,7 +79,8 @@ def half_update_error(which, n, warm_sweeps):
             e1.record()
             torch.cuda.synchronize()
             d[tag + "_pairs_per_s"] = 3.0 * dev.n * dev.m / (e0.elapsed_time(e1) * 1e-3)
-        os.environ.pop("CNTGW_CTR_TC", None)
+        for key in ("CNTGW_CTR_TC", "CNTGW_CTR_SKIP"):
+            os.environ.pop(key, None)
         for tag, _, _ in variants[1:]:
             e = ((res[tag] - res["f64"]).abs() * lam).cpu().numpy()
             d[tag] = dict(max=float(e.max()), p99=float(np.percentile(e, 99)), median=float(np.median(e)),
