@@ -171,9 +171,9 @@ KernelPick pick_tc() {
 
 // CNTGW_F32C: centred fp32 pairs over locality-ordered tiles (softmin_ctr.cuh);
 // KX = kd + sq padded to 4 (8 rows per thread) or 8 (4 rows per thread).
-template <int KX>
+template <int KX, int R = (KX <= 4 ? 8 : 4)>
 KernelPick pick_ctr() {
-  constexpr int R = KX <= 4 ? 8 : 4, MINB = KX <= 4 ? 4 : 3;
+  constexpr int MINB = KX <= 4 ? (R <= 4 ? 6 : 4) : 3;
   KernelPick k;
   // tuning alternatives (tools/ctr_check.py): CNTGW_CTR_POLY row pairs per
   // 4-column group on the FMA-pipe exp2; CNTGW_CTR_MINB=3 trades a CTA per SM
@@ -231,7 +231,8 @@ bool lookup(int prec, int kd, int sq, KernelPick* out) {
     if (!kd_supported(kd)) return false;
     const int kx = kd + (sq ? 1 : 0);
     if (kx <= 4 && env_int("CNTGW_CTR_TC", 0)) { *out = pick_ctc(); return true; }
-    if (kx <= 4) { *out = pick_ctr<4>(); return true; }
+    // CNTGW_CTR_R=4: 4 row groups per CTA (finer block-sparse granularity)
+    if (kx <= 4) { *out = env_int("CNTGW_CTR_R", 8) == 4 ? pick_ctr<4, 4>() : pick_ctr<4>(); return true; }
     if (kx <= 8) { *out = pick_ctr<8>(); return true; }
     return false;
   }
@@ -649,8 +650,10 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
     uint8_t* need = reinterpret_cast<uint8_t*>(rho) + align256(sizeof(float) * ctas * k.ctr_r * tl);
     const char* e = getenv("CNTGW_CTR_SKIP_T");
     const double T = e ? atof(e) : 64.0;
-    if (k.ctr_kx == 4)
+    if (k.ctr_kx == 4 && k.ctr_r == 8)
       ctr_plan_kernel<4, 8><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, T);
+    else if (k.ctr_kx == 4)
+      ctr_plan_kernel<4, 4><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, T);
     else
       ctr_plan_kernel<8, 4><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, T);
     a.ctr_need = need;
