@@ -168,7 +168,11 @@ int cntgw_prep_cols(const cntgw_sweep_state* st, int prec, int kd, int sq_flag, 
  * the column block is per half-update (it holds lam and pot). cntgw_softmin
  * with prec = CNTGW_F32C then takes row_feat = the row block, row_sq = the
  * rows' fp64 squared coordinate in the caller's order (or NULL without sq),
- * col_rec = the column block; outputs are in the caller's order. */
+ * col_rec = the column block; outputs are in the caller's order. Its
+ * workspace (cntgw_softmin_workspace) also holds a block-sparse plan: a first
+ * kernel bounds every (row group, column tile) pair and the sweep skips the
+ * tiles that cannot hold a term within 2^-64 of any of its rows' maxima
+ * (CNTGW_CTR_SKIP=0 disables it). */
 int cntgw_locality_codes(const double* x, int64_t n, int d, int64_t ld, double* bbox, int64_t* codes,
                          void* stream);
 size_t cntgw_ctr_rows_bytes(int64_t n, int kd, int sq_flag);

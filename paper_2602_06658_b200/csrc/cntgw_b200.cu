@@ -202,7 +202,7 @@ size_t ctr_plan_bytes(const KernelPick& k, int64_t n, int64_t m) {
   if (!ctr_skip_enabled(k)) return 0;
   const int64_t ctas = (ctr_groups(n) + k.ctr_r - 1) / k.ctr_r;
   const int64_t tl = (m + kColTile - 1) / kColTile;
-  return align256(sizeof(float) * ctas * k.ctr_r * tl) + align256((size_t)(ctas * tl));
+  return align256(sizeof(float) * ctas * k.ctr_r * tl) + align256(sizeof(uint32_t) * ctas * tl);
 }
 
 // CNTGW_F32C, kx <= 4, on tcgen05 (softmin_ctr_tc.cuh), opt-in with CNTGW_CTR_TC=1:
@@ -231,8 +231,9 @@ bool lookup(int prec, int kd, int sq, KernelPick* out) {
     if (!kd_supported(kd)) return false;
     const int kx = kd + (sq ? 1 : 0);
     if (kx <= 4 && env_int("CNTGW_CTR_TC", 0)) { *out = pick_ctc(); return true; }
-    // CNTGW_CTR_R=4: 4 row groups per CTA (finer block-sparse granularity)
-    if (kx <= 4) { *out = env_int("CNTGW_CTR_R", 8) == 4 ? pick_ctr<4, 4>() : pick_ctr<4>(); return true; }
+    // 4 row groups per CTA (finer block-sparse granularity, and faster dense:
+    // 3.3e12 vs 3.14e12 at the C4 law); CNTGW_CTR_R=8 for the 8-group CTA
+    if (kx <= 4) { *out = env_int("CNTGW_CTR_R", 4) == 8 ? pick_ctr<4, 8>() : pick_ctr<4, 4>(); return true; }
     if (kx <= 8) { *out = pick_ctr<8>(); return true; }
     return false;
   }
@@ -647,15 +648,18 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
   if (plan_bytes > 0) {  // block-sparse plan of the centred kernel (ctr_plan_kernel)
     const int64_t ctas = (ctr_groups(n) + k.ctr_r - 1) / k.ctr_r, tl = (m + kColTile - 1) / kColTile;
     float* rho = reinterpret_cast<float*>(static_cast<char*>(workspace) + part_bytes);
-    uint8_t* need = reinterpret_cast<uint8_t*>(rho) + align256(sizeof(float) * ctas * k.ctr_r * tl);
+    uint32_t* need = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(rho) +
+                                                 align256(sizeof(float) * ctas * k.ctr_r * tl));
     const char* e = getenv("CNTGW_CTR_SKIP_T");
     const double T = e ? atof(e) : 64.0;
+    // one planning block per streaming CTA (S = 1: planning 4 CTAs per block
+    // to share the column reads measured 2.6x slower, 43 vs 17 ms at 2^20)
     if (k.ctr_kx == 4 && k.ctr_r == 8)
-      ctr_plan_kernel<4, 8><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, T);
+      ctr_plan_kernel<4, 8, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, T);
     else if (k.ctr_kx == 4)
-      ctr_plan_kernel<4, 4><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, T);
+      ctr_plan_kernel<4, 4, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, T);
     else
-      ctr_plan_kernel<8, 4><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, T);
+      ctr_plan_kernel<8, 4, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, T);
     a.ctr_need = need;
   }
   void* args[] = {&a};

@@ -49,7 +49,7 @@ struct SoftminArgs {
   double* part_max;  // [nchunks][n] split-column partials (nchunks > 1)
   double* part_sum;
   double ctr_limit;  // CNTGW_F32C: per-(group, tile) bound on the fp32 pair term
-  const uint8_t* ctr_need;  // CNTGW_F32C: [CTA][tile] needed-tile mask (ctr_plan_kernel) or null
+  const uint32_t* ctr_need;  // CNTGW_F32C: [CTA][tile] needed-tile votes (ctr_plan_kernel) or null
 };
 
 template <typename T, int KD, int SQ>

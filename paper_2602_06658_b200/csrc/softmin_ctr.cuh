@@ -392,8 +392,8 @@ __global__ void __launch_bounds__(128, MINB) softmin_ctr_kernel(const SoftminArg
   // Block-sparse plan (ctr_plan_kernel): tiles that cannot hold a term within
   // 2^-T of any of this CTA's rows' maxima are skipped; every thread walks the
   // same sequence of needed tiles (a uniform scan of a byte mask in L1/L2).
-  const uint8_t* need = a.ctr_need ? a.ctr_need + (int64_t)blockIdx.x * (mpad / kColTile) + c0 / kColTile
-                                   : nullptr;
+  const uint32_t* need = a.ctr_need ? a.ctr_need + (int64_t)blockIdx.x * (mpad / kColTile) + c0 / kColTile
+                                    : nullptr;
   auto next_needed = [&](int t) {
     if (need)
       while (t < ntiles && !need[t]) ++t;
@@ -558,94 +558,103 @@ __global__ void __launch_bounds__(128, MINB) softmin_ctr_kernel(const SoftminArg
 // tiles: rho_IJ = min_j A_j^I (fp64, as the streaming prologue), per row
 // B_i^J, and the bounds on the row's terms in tile J (log2 units, t = -q)
 //     t_ij <= -(rho_IJ + B_i^J) + C_IJ,   max_j t_ij >= -(rho_IJ + B_i^J) - C_IJ,
-// C_IJ = R_I R_J the pair-term bound. Pass 1 keeps L_i = max_J of the lower
-// bound and rho (rounded down to fp32: only loosens the upper bound); pass 2
-// marks tile J needed for the CTA when some row has an upper bound above
+// C_IJ = R_I R_J the pair-term bound. (1) each warp takes every 4th tile and
+// reduces rho over its 256 columns (no block barrier per tile), stored in fp32
+// rounded down; (2) every row keeps L_i = max_J of the lower bound (with rho
+// rounded back up, so it stays a lower bound); (3) a warp votes tile J needed
+// when one of its 32 rows has an upper bound (rho rounded down) reaching
 // L_i - T. A skipped tile holds only terms below 2^-T of its row's maximum,
-// so with T = 64 the skipped mass is < m 2^-64 of every row's sum.
-template <int KX, int R>
-__global__ void __launch_bounds__(128) ctr_plan_kernel(const SoftminArgs a, float* rho_tab, uint8_t* need,
+// so with T = 64 the skipped mass is < m 2^-64 of every row's sum. need:
+// [CTA][tile] 32-bit words, one vote byte per warp.
+template <int KX, int R, int S>
+__global__ void __launch_bounds__(128) ctr_plan_kernel(const SoftminArgs a, float* rho_tab, uint32_t* need,
                                                        double T) {
-  __shared__ double gctr[R][KX];
-  __shared__ double grad[R];
-  __shared__ double red[4][R];
+  // one block plans S consecutive streaming CTAs (S * R row groups): each
+  // column record is read once per S * R groups
+  constexpr int GB = S * R;
+  __shared__ double gctr[GB][KX];
+  __shared__ double grad[GB];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t mpad = (a.m + kColTile - 1) / kColTile * kColTile;
   const int64_t TL = mpad / kColTile;
   const CtrRows rows = ctr_rows_view(a.row_feat, a.n, KX);
   const CtrCols cols = ctr_cols_view(a.col_rec, mpad, KX);
-  const int64_t g0 = (int64_t)blockIdx.x * R;
   const int64_t ngroups = ctr_groups(a.n);
-  if (tid < R * KX) {
-    const int r = tid / KX, k = tid % KX;
+  const int64_t nctas = (ngroups + R - 1) / R;
+  const int64_t cta0 = (int64_t)blockIdx.x * S, g0 = cta0 * R;
+  for (int e = tid; e < GB * KX; e += blockDim.x) {
+    const int r = e / KX, k = e % KX;
     gctr[r][k] = g0 + r < ngroups ? rows.ctr[(g0 + r) * (KX + 1) + k] : 0.0;
   }
-  if (tid < R) grad[tid] = g0 + tid < ngroups ? rows.ctr[(g0 + tid) * (KX + 1) + KX] : 0.0;
+  if (tid < GB) grad[tid] = g0 + tid < ngroups ? rows.ctr[(g0 + tid) * (KX + 1) + KX] : 0.0;
   __syncthreads();
-  double dx[R][KX];
+  float* rho_blk = rho_tab + g0 * TL;  // [group][tile], groups of consecutive CTAs are contiguous
+  for (int64_t J = warp; J < TL; J += 4) {  // (1) rho, one tile per warp
+    double mn[GB];
 #pragma unroll
-  for (int r = 0; r < R; ++r)
-#pragma unroll
-    for (int k = 0; k < KX; ++k)
-      dx[r][k] = g0 + r < ngroups ? rows.dx64[((g0 + r) * kCtrRowGroup + tid) * KX + k] : 0.0;
-  double L[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) L[r] = -CUDART_INF;
-  float* rho_cta = rho_tab + (int64_t)blockIdx.x * R * TL;
-  for (int64_t J = 0; J < TL; ++J) {  // pass 1
-    double A[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) A[r] = CUDART_INF;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const double* rj = cols.rec64 + (J * kColTile + tid + 128 * h) * (KX + 1);
+    for (int r = 0; r < GB; ++r) mn[r] = CUDART_INF;
+#pragma unroll 4
+    for (int u = 0; u < kColTile / 32; ++u) {
+      const double* rj = cols.rec64 + (J * kColTile + lane + 32 * u) * (KX + 1);
       double z[KX];
 #pragma unroll
       for (int k = 0; k < KX; ++k) z[k] = rj[k];
       const double c = rj[KX];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
+      for (int r = 0; r < GB; ++r) {
         double acc = c;
 #pragma unroll
         for (int k = 0; k < KX; ++k) acc = fma(gctr[r][k], z[k], acc);
-        A[r] = fmin(A[r], acc);
+        mn[r] = fmin(mn[r], acc);
       }
     }
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      double v = A[r];
+    for (int r = 0; r < GB; ++r) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
-      if (lane == 0) red[warp][r] = v;
+      for (int o = 16; o > 0; o >>= 1) mn[r] = fmin(mn[r], __shfl_xor_sync(0xffffffffu, mn[r], o));
+      if (lane == r % 32 && g0 + r < ngroups) rho_blk[r * TL + J] = __double2float_rd(mn[r]);
     }
-    __syncthreads();
-    const double* tc = cols.tctr + J * (KX + 1);
-    const double radJ = tc[KX];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const double rho = fmin(fmin(red[0][r], red[1][r]), fmin(red[2][r], red[3][r]));
-      double b = rho;
-#pragma unroll
-      for (int k = 0; k < KX; ++k) b = fma(dx[r][k], tc[k], b);
-      L[r] = fmax(L[r], -b - grad[r] * radJ);  // (+inf rho: zero-weight tile, no bound)
-      if (tid == 0) rho_cta[r * TL + J] = __double2float_rd(rho);
-    }
-    __syncthreads();  // red[] reuse
   }
-  __syncthreads();  // rho_cta visible to the block
-  for (int64_t J = 0; J < TL; ++J) {  // pass 2
-    const double* tc = cols.tctr + J * (KX + 1);
-    const double radJ = tc[KX];
-    int keep = 0;
+  __syncthreads();  // rho_blk visible to the block
+  for (int sc = 0; sc < S && cta0 + sc < nctas; ++sc) {
+    const int r0 = sc * R;
+    double dx[R][KX], L[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      double b = (double)rho_cta[r * TL + J];
 #pragma unroll
-      for (int k = 0; k < KX; ++k) b = fma(dx[r][k], tc[k], b);
-      keep |= (g0 + r < ngroups) && (-b + grad[r] * radJ >= L[r] - T);
+      for (int k = 0; k < KX; ++k)
+        dx[r][k] = g0 + r0 + r < ngroups ? rows.dx64[((g0 + r0 + r) * kCtrRowGroup + tid) * KX + k] : 0.0;
+      L[r] = -CUDART_INF;
     }
-    keep = __syncthreads_or(keep);
-    if (tid == 0) need[(int64_t)blockIdx.x * TL + J] = (uint8_t)keep;
+    for (int64_t J = 0; J < TL; ++J) {  // (2) L_i
+      const double* tc = cols.tctr + J * (KX + 1);
+      const double radJ = tc[KX];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (g0 + r0 + r >= ngroups) break;
+        const double rd = (double)rho_blk[(r0 + r) * TL + J];
+        double b = rd + fabs(rd) * 0x1p-23;  // >= the exact rho: a valid lower bound below
+#pragma unroll
+        for (int k = 0; k < KX; ++k) b = fma(dx[r][k], tc[k], b);
+        L[r] = fmax(L[r], -b - grad[r0 + r] * radJ);  // (+inf rho: zero-weight tile, no bound)
+      }
+    }
+    uint8_t* vote = reinterpret_cast<uint8_t*>(need + (cta0 + sc) * TL);
+    for (int64_t J = 0; J < TL; ++J) {  // (3) verdicts
+      const double* tc = cols.tctr + J * (KX + 1);
+      const double radJ = tc[KX];
+      bool keep = false;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (g0 + r0 + r >= ngroups) break;
+        double b = (double)rho_blk[(r0 + r) * TL + J];
+#pragma unroll
+        for (int k = 0; k < KX; ++k) b = fma(dx[r][k], tc[k], b);
+        keep |= -b + grad[r0 + r] * radJ >= L[r] - T;
+      }
+      keep = __any_sync(0xffffffffu, keep);
+      if (lane == 0) vote[J * 4 + warp] = keep ? 1 : 0;
+    }
   }
 }
 
