@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kCtrRowGroup) prep_rows_ctr_kernel(
 // lazily rebased MUFU.EX2 sums as softmin_tile_f32.
 // POLY: row pairs (of the first column of each group) whose exp2 runs on the
 // FMA pipe (exp2_poly2) instead of MUFU, balancing the two pipes.
-template <int KX, int R, int G, int POLY>
+template <int KX, int R, int G, int POLY, int PM = (1 << (R / 2)) - 1>
 __device__ __forceinline__ void softmin_tile_ctr(const float* __restrict__ rec,
                                                  const float* __restrict__ bias,
                                                  const float2 (&x2)[R / 2][KX], float (&mq)[R],
@@ -274,6 +274,7 @@ __device__ __forceinline__ void softmin_tile_ctr(const float* __restrict__ rec,
       }
 #pragma unroll
       for (int p = 0; p < P; ++p) {
+        if (!((PM >> p) & 1)) continue;  // row pair without a needed group (block-sparse plan)
         float2 acc = f2(bv[2 * p], bv[2 * p + 1]);
 #pragma unroll
         for (int k = 0; k < KX; ++k) acc = fma2(x2[p][k], f2(c[k], c[k]), acc);
@@ -282,6 +283,7 @@ __device__ __forceinline__ void softmin_tile_ctr(const float* __restrict__ rec,
     }
 #pragma unroll
     for (int p = 0; p < P; ++p) {
+      if (!((PM >> p) & 1)) continue;
       const float2 m2 = f2(mq[2 * p], mq[2 * p + 1]);
       float2 gs = f2(0.f, 0.f);
 #pragma unroll
@@ -316,6 +318,7 @@ __device__ __forceinline__ void softmin_tile_ctr(const float* __restrict__ rec,
   }
 #pragma unroll
   for (int p = 0; p < P; ++p) {
+    if (!((PM >> p) & 1)) continue;
     S[2 * p] += f32_to_f64_alu(T[p].x);
     S[2 * p + 1] += f32_to_f64_alu(T[p].y);
   }
@@ -488,7 +491,19 @@ __global__ void __launch_bounds__(128, MINB) softmin_ctr_kernel(const SoftminArg
     float mq0[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) mq0[r] = mq[r];
-    softmin_tile_ctr<KX, R, G, POLY>(s32 + s * SM::kStage32, sbias, x2, mq, S);
+    if constexpr (R == 4) {  // skip a row pair none of whose groups needs the tile
+      uint32_t v = need ? need[tq[s]] : 0xFFu;
+      v = (v | (v >> 8) | (v >> 16) | (v >> 24)) & 0xFu;
+      const int pm = ((v & 3u) ? 1 : 0) | ((v & 12u) ? 2 : 0);
+      if (pm == 1)
+        softmin_tile_ctr<KX, R, G, POLY, 1>(s32 + s * SM::kStage32, sbias, x2, mq, S);
+      else if (pm == 2)
+        softmin_tile_ctr<KX, R, G, POLY, 2>(s32 + s * SM::kStage32, sbias, x2, mq, S);
+      else
+        softmin_tile_ctr<KX, R, G, POLY>(s32 + s * SM::kStage32, sbias, x2, mq, S);
+    } else {
+      softmin_tile_ctr<KX, R, G, POLY>(s32 + s * SM::kStage32, sbias, x2, mq, S);
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (mq[r] != mq0[r]) sM[r * 128 + tid] = sOff[r * 128 + tid] + (double)mq[r];
@@ -565,7 +580,7 @@ __global__ void __launch_bounds__(128, MINB) softmin_ctr_kernel(const SoftminArg
 // when one of its 32 rows has an upper bound (rho rounded down) reaching
 // L_i - T. A skipped tile holds only terms below 2^-T of its row's maximum,
 // so with T = 64 the skipped mass is < m 2^-64 of every row's sum. need:
-// [CTA][tile] 32-bit words, one vote byte per warp.
+// [CTA][tile] 32-bit words, one byte per warp whose bit r votes for group r.
 template <int KX, int R, int S>
 __global__ void __launch_bounds__(128) ctr_plan_kernel(const SoftminArgs a, float* rho_tab, uint32_t* need,
                                                        double T) {
@@ -616,44 +631,58 @@ __global__ void __launch_bounds__(128) ctr_plan_kernel(const SoftminArgs a, floa
     }
   }
   __syncthreads();  // rho_blk visible to the block
+  // (2)/(3) in fp32 with an explicit rounding allowance: every quantity is a
+  // bound, so it is enough that the lower bound is rounded down and the upper
+  // one up; err = (|rho| + |B| + C) 2^-20 covers the fp32 roundings of rho
+  // (stored rounded down), of B = <dx, Zc> and of the sums.
   for (int sc = 0; sc < S && cta0 + sc < nctas; ++sc) {
     const int r0 = sc * R;
-    double dx[R][KX], L[R];
+    float dx[R][KX], L[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
 #pragma unroll
       for (int k = 0; k < KX; ++k)
-        dx[r][k] = g0 + r0 + r < ngroups ? rows.dx64[((g0 + r0 + r) * kCtrRowGroup + tid) * KX + k] : 0.0;
-      L[r] = -CUDART_INF;
+        dx[r][k] = g0 + r0 + r < ngroups ? (float)rows.dx64[((g0 + r0 + r) * kCtrRowGroup + tid) * KX + k] : 0.f;
+      L[r] = -CUDART_INF_F;
     }
     for (int64_t J = 0; J < TL; ++J) {  // (2) L_i
       const double* tc = cols.tctr + J * (KX + 1);
-      const double radJ = tc[KX];
+      float zc[KX];
+#pragma unroll
+      for (int k = 0; k < KX; ++k) zc[k] = (float)tc[k];
+      const float radJ = (float)tc[KX];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (g0 + r0 + r >= ngroups) break;
-        const double rd = (double)rho_blk[(r0 + r) * TL + J];
-        double b = rd + fabs(rd) * 0x1p-23;  // >= the exact rho: a valid lower bound below
+        const float rd = rho_blk[(r0 + r) * TL + J];
+        float bb = 0.f;
 #pragma unroll
-        for (int k = 0; k < KX; ++k) b = fma(dx[r][k], tc[k], b);
-        L[r] = fmax(L[r], -b - grad[r0 + r] * radJ);  // (+inf rho: zero-weight tile, no bound)
+        for (int k = 0; k < KX; ++k) bb = fmaf(dx[r][k], zc[k], bb);
+        const float cc = (float)grad[r0 + r] * radJ;
+        const float err = (fabsf(rd) + fabsf(bb) + cc) * 0x1p-20f;
+        L[r] = fmaxf(L[r], -(rd + bb) - cc - err);  // (+inf rho: zero-weight tile, no bound)
       }
     }
     uint8_t* vote = reinterpret_cast<uint8_t*>(need + (cta0 + sc) * TL);
     for (int64_t J = 0; J < TL; ++J) {  // (3) verdicts
       const double* tc = cols.tctr + J * (KX + 1);
-      const double radJ = tc[KX];
-      bool keep = false;
+      float zc[KX];
+#pragma unroll
+      for (int k = 0; k < KX; ++k) zc[k] = (float)tc[k];
+      const float radJ = (float)tc[KX];
+      uint32_t keep = 0;  // bit r: group r needs the tile
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (g0 + r0 + r >= ngroups) break;
-        double b = (double)rho_blk[(r0 + r) * TL + J];
+        const float rd = rho_blk[(r0 + r) * TL + J];
+        float bb = 0.f;
 #pragma unroll
-        for (int k = 0; k < KX; ++k) b = fma(dx[r][k], tc[k], b);
-        keep |= -b + grad[r0 + r] * radJ >= L[r] - T;
+        for (int k = 0; k < KX; ++k) bb = fmaf(dx[r][k], zc[k], bb);
+        const float cc = (float)grad[r0 + r] * radJ;
+        const float err = (fabsf(rd) + fabsf(bb) + cc) * 0x1p-20f;
+        keep |= (__any_sync(0xffffffffu, -(rd + bb) + cc + err >= L[r] - (float)T) ? 1u : 0u) << r;
       }
-      keep = __any_sync(0xffffffffu, keep);
-      if (lane == 0) vote[J * 4 + warp] = keep ? 1 : 0;
+      if (lane == 0) vote[J * 4 + warp] = (uint8_t)keep;
     }
   }
 }
