@@ -107,9 +107,11 @@ def exponent_scale(eps: float, feat_r, sq_r, feat_c, sq_c, pot_abs: float = 0.0)
 CTR_TILE_LIMIT = float(os.environ.get("CNTGW_CTR_TILE_LIMIT", 65536.0))
 CTR_MAX_DEFERRED = 0.05
 # ... and only for half-updates of at least this many pairs: below it the
-# fp64 kernels take well under a millisecond and keep fp64-level agreement
-# with the reference's discrete decisions (threshold stops, divergence guard)
-CTR_MIN_PAIRS = float(os.environ.get("CNTGW_CTR_MIN_PAIRS", 2.0 ** 28))
+# fp64 kernels take a few milliseconds, the planning pass and the per-step
+# path decision do not pay off (C3, 1e10 pairs: 1.72 s centred vs 1.08 s
+# fp64), and fp64 keeps fp64-level agreement with the reference's discrete
+# decisions (threshold stops, divergence guard)
+CTR_MIN_PAIRS = float(os.environ.get("CNTGW_CTR_MIN_PAIRS", 2.0 ** 34))
 CTR_ROW_GROUP, CTR_COL_TILE = 128, 256
 
 
