@@ -175,18 +175,13 @@ template <int KX, int R = (KX <= 4 ? 8 : 4)>
 KernelPick pick_ctr() {
   constexpr int MINB = KX <= 4 ? (R <= 4 ? 6 : 4) : 3;
   KernelPick k;
-  // tuning alternatives (tools/ctr_check.py): CNTGW_CTR_POLY row pairs per
-  // 4-column group on the FMA-pipe exp2; CNTGW_CTR_MINB=3 trades a CTA per SM
-  // for registers
-  const int poly = env_int("CNTGW_CTR_POLY", 0), minb3 = env_int("CNTGW_CTR_MINB", MINB) == 3;
-  if (minb3)
-    k.fn = poly == 1 ? (void*)softmin_ctr_kernel<KX, R, 4, 3, 1>
-         : poly == 2 ? (void*)softmin_ctr_kernel<KX, R, 4, 3, 2>
-                     : (void*)softmin_ctr_kernel<KX, R, 4, 3, 0>;
-  else
-    k.fn = poly == 1 ? (void*)softmin_ctr_kernel<KX, R, 4, MINB, 1>
-         : poly == 2 ? (void*)softmin_ctr_kernel<KX, R, 4, MINB, 2>
-                     : (void*)softmin_ctr_kernel<KX, R, 4, MINB, 0>;
+  // tuning alternatives (tools/ctr_check.py): CNTGW_CTR_POLY=1 puts one row
+  // pair of each column group on the FMA-pipe exp2; CNTGW_CTR_G=8 checks the
+  // lazy rebase once per 8 columns instead of 4
+  const int poly = env_int("CNTGW_CTR_POLY", 0), g8 = env_int("CNTGW_CTR_G", 4) == 8;
+  k.fn = g8 ? (void*)softmin_ctr_kernel<KX, R, 8, MINB, 0>
+       : poly == 1 ? (void*)softmin_ctr_kernel<KX, R, 4, MINB, 1>
+                   : (void*)softmin_ctr_kernel<KX, R, 4, MINB, 0>;
   k.rows = R;
   k.smem = CtrSmem<KX, R>::kBytes;
   k.rec_bytes = (KX + 1) * sizeof(double) + KX * sizeof(float);
