@@ -172,7 +172,9 @@ int cntgw_prep_cols(const cntgw_sweep_state* st, int prec, int kd, int sq_flag, 
  * workspace (cntgw_softmin_workspace) also holds a block-sparse plan: a first
  * kernel bounds every (row group, column tile) pair and the sweep skips the
  * tiles that cannot hold a term within 2^-64 of any of its rows' maxima
- * (CNTGW_CTR_SKIP=0 disables it). */
+ * (CNTGW_CTR_SKIP=0 disables it); the plan is reused across the sweeps of a
+ * loop (st->sweep > 1) while no column record moved by more than its margin
+ * (CNTGW_CTR_REUSE=0 replans every call). */
 int cntgw_locality_codes(const double* x, int64_t n, int d, int64_t ld, double* bbox, int64_t* codes,
                          void* stream);
 size_t cntgw_ctr_rows_bytes(int64_t n, int kd, int sq_flag);

@@ -197,7 +197,8 @@ size_t ctr_plan_bytes(const KernelPick& k, int64_t n, int64_t m) {
   if (!ctr_skip_enabled(k)) return 0;
   const int64_t ctas = (ctr_groups(n) + k.ctr_r - 1) / k.ctr_r;
   const int64_t tl = (m + kColTile - 1) / kColTile;
-  return align256(sizeof(float) * ctas * k.ctr_r * tl) + align256(sizeof(uint32_t) * ctas * tl);
+  return align256(sizeof(float) * ctas * k.ctr_r * tl) + align256(sizeof(uint32_t) * ctas * tl) +
+         align256(sizeof(double) * tl * kColTile) + 256;  // + c at the last plan, replan flag
 }
 
 // CNTGW_F32C, kx <= 4, on tcgen05 (softmin_ctr_tc.cuh), opt-in with CNTGW_CTR_TC=1:
@@ -645,16 +646,34 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
     float* rho = reinterpret_cast<float*>(static_cast<char*>(workspace) + part_bytes);
     uint32_t* need = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(rho) +
                                                  align256(sizeof(float) * ctas * k.ctr_r * tl));
+    double* c_plan = reinterpret_cast<double*>(reinterpret_cast<char*>(need) +
+                                               align256(sizeof(uint32_t) * ctas * tl));
+    int* replan = reinterpret_cast<int*>(reinterpret_cast<char*>(c_plan) + align256(sizeof(double) * tl * kColTile));
     const char* e = getenv("CNTGW_CTR_SKIP_T");
     const double T = e ? atof(e) : 64.0;
+    // plans are reused across sweeps while the column records moved by at
+    // most `budget` log2 units (CNTGW_CTR_REUSE=0: replan every half-update)
+    const double budget = 8.0;
+    const bool reuse = env_int("CNTGW_CTR_REUSE", 1) != 0;
+    const int64_t mp = tl * kColTile;
+    const CtrCols cv = ctr_cols_view(col_rec, mp, k.ctr_kx);
+    const int* rp = nullptr;
+    if (reuse) {
+      if (k.ctr_kx == 4)
+        ctr_plan_check_kernel<4><<<1, 1024, 0, s>>>(st, cv.rec64, mp, c_plan, replan, budget);
+      else
+        ctr_plan_check_kernel<8><<<1, 1024, 0, s>>>(st, cv.rec64, mp, c_plan, replan, budget);
+      rp = replan;
+    }
+    const double Tp = reuse ? T + 2.0 * budget : T;
     // one planning block per streaming CTA (S = 1: planning 4 CTAs per block
     // to share the column reads measured 2.6x slower, 43 vs 17 ms at 2^20)
     if (k.ctr_kx == 4 && k.ctr_r == 8)
-      ctr_plan_kernel<4, 8, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, T);
+      ctr_plan_kernel<4, 8, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, Tp, rp);
     else if (k.ctr_kx == 4)
-      ctr_plan_kernel<4, 4, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, T);
+      ctr_plan_kernel<4, 4, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, Tp, rp);
     else
-      ctr_plan_kernel<8, 4, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, T);
+      ctr_plan_kernel<8, 4, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, Tp, rp);
     a.ctr_need = need;
   }
   void* args[] = {&a};

@@ -581,9 +581,45 @@ __global__ void __launch_bounds__(128, MINB) softmin_ctr_kernel(const SoftminArg
 // L_i - T. A skipped tile holds only terms below 2^-T of its row's maximum,
 // so with T = 64 the skipped mass is < m 2^-64 of every row's sum. need:
 // [CTA][tile] 32-bit words, one byte per warp whose bit r votes for group r.
+// Plan reuse across sweeps. Column potentials move every sweep, but every
+// term t_ij of a half-update shifts by exactly the change of its column's c_j
+// (log2 units; rows' own potentials do not enter), so a plan made with
+// threshold T + 2 budget stays valid while max_j |c_j - c_j(plan)| <= budget
+// and the features are unchanged (they change only between Sinkhorn loops:
+// the first sweep of a loop always replans). One block compares the current
+// column records with the copy taken at the last plan and sets *replan.
+template <int KX>
+__global__ void __launch_bounds__(1024) ctr_plan_check_kernel(const cntgw_sweep_state* st, const double* rec64,
+                                                              int64_t mpad, double* c_plan, int* replan,
+                                                              double budget) {
+  __shared__ double red[32];
+  __shared__ int go;
+  const bool first = st == nullptr || st->sweep <= 1;
+  double d = 0.0;
+  if (!first)
+    for (int64_t j = threadIdx.x; j < mpad; j += blockDim.x) {
+      const double c = rec64[j * (KX + 1) + KX], cp = c_plan[j];
+      d = fmax(d, c == cp ? 0.0 : fabs(c - cp));  // (equal infinities: no change; NaN -> replan below)
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = d;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) m = fmax(m, red[q]);
+    go = (first || !(m <= budget)) ? 1 : 0;
+    *replan = go;
+  }
+  __syncthreads();
+  if (go)
+    for (int64_t j = threadIdx.x; j < mpad; j += blockDim.x) c_plan[j] = rec64[j * (KX + 1) + KX];
+}
+
 template <int KX, int R, int S>
 __global__ void __launch_bounds__(128) ctr_plan_kernel(const SoftminArgs a, float* rho_tab, uint32_t* need,
-                                                       double T) {
+                                                       double T, const int* replan) {
+  if (replan && !*replan) return;  // the previous plan still holds (ctr_plan_check_kernel)
   // one block plans S consecutive streaming CTAs (S * R row groups): each
   // column record is read once per S * R groups
   constexpr int GB = S * R;
