@@ -294,3 +294,31 @@ def test_low_rank_paths(env, prec, k, n, m):
     want = O.softmin(O.LowRank(inst.u, inst.v, inst.row_sep, inst.col_sep), np.log(b),
                      inst.g.astype(float) + inst.col_sep, inst.eps)
     assert _rel(got, want) < 1e-5
+
+
+def test_centred_plan_reuse_across_sweeps(env, monkeypatch):
+    """A Sinkhorn loop on the centred path reuses its block-sparse plan across
+    sweeps while no column record moved by more than the plan's margin: the
+    potentials equal those of replanning every half-update (to 1e-9) and of
+    the dense sweep."""
+    P, engine, S, O, torch, dev = env
+    rng = np.random.default_rng(21)
+    n = m = 1 << 15
+    cx = rng.standard_normal((8, 3)) * 2.0
+    x = cx[rng.integers(0, 8, n)] + rng.standard_normal((n, 3)) * 0.7
+    z = cx[rng.integers(0, 8, m)] + rng.standard_normal((m, 3)) * 0.7
+    a, b = np.full(n, 1 / n), np.full(m, 1 / m)
+    monkeypatch.setenv("CNTGW_PRECISION", "f32c")
+    cfg = P.SinkhornConfig(eps=2e-3, n_inner=30)
+    out = {}
+    for tag, env_vars in (("reuse", {}), ("replan", {"CNTGW_CTR_REUSE": "0"}),
+                          ("dense", {"CNTGW_CTR_SKIP": "0"})):
+        for key in ("CNTGW_CTR_REUSE", "CNTGW_CTR_SKIP"):
+            monkeypatch.delenv(key, raising=False)
+        for key, val in env_vars.items():
+            monkeypatch.setenv(key, val)
+        res = P.sinkhorn(a, b, P.SquaredEuclideanCost(x, z), cfg)
+        out[tag] = (res.coupling.f, res.coupling.g)
+    for tag in ("replan", "dense"):
+        assert _rel(out["reuse"][0], out[tag][0]) < 1e-9, tag
+        assert _rel(out["reuse"][1], out[tag][1]) < 1e-9, tag
