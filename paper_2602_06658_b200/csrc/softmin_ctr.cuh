@@ -21,7 +21,10 @@
 // tile the group biases a_j = fp32(A_j^I - min_j A_j^I) are written to shared
 // memory, and the row's fp64 reference M_i enters the tile as the fp32 offset
 // fp32(M_i - min A - B_i). Rows are processed in locality order and their
-// results scattered back to the caller's order.
+// results scattered back to the caller's order. A (group, tile) pair whose
+// pair-term bound exceeds ctr_limit runs in fp64 in the same kernel, and a
+// planning pass (ctr_plan_kernel, below) lets the sweep skip the tiles that
+// cannot hold a term within 2^-64 of any of the CTA's rows' maxima.
 #pragma once
 
 #include "common.cuh"
