@@ -228,8 +228,13 @@ bool lookup(int prec, int kd, int sq, KernelPick* out) {
     const int kx = kd + (sq ? 1 : 0);
     if (kx <= 4 && env_int("CNTGW_CTR_TC", 0)) { *out = pick_ctc(); return true; }
     // 4 row groups per CTA (finer block-sparse granularity, and faster dense:
-    // 3.3e12 vs 3.14e12 at the C4 law); CNTGW_CTR_R=8 for the 8-group CTA
-    if (kx <= 4) { *out = env_int("CNTGW_CTR_R", 4) == 8 ? pick_ctr<4, 8>() : pick_ctr<4, 4>(); return true; }
+    // 3.3e12 vs 3.14e12 at the C4 law); CNTGW_CTR_R=8 / 2 for 8 / 2 groups
+    // (2 groups: 12.8e12 vs 14.8e12 N*M pairs/s 100 sweeps into C4)
+    if (kx <= 4) {
+      const int r = env_int("CNTGW_CTR_R", 4);
+      *out = r == 8 ? pick_ctr<4, 8>() : (r == 2 ? pick_ctr<4, 2>() : pick_ctr<4, 4>());
+      return true;
+    }
     if (kx <= 8) { *out = pick_ctr<8>(); return true; }
     return false;
   }
@@ -670,6 +675,8 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
     // to share the column reads measured 2.6x slower, 43 vs 17 ms at 2^20)
     if (k.ctr_kx == 4 && k.ctr_r == 8)
       ctr_plan_kernel<4, 8, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, Tp, rp);
+    else if (k.ctr_kx == 4 && k.ctr_r == 2)
+      ctr_plan_kernel<4, 2, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, Tp, rp);
     else if (k.ctr_kx == 4)
       ctr_plan_kernel<4, 4, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, Tp, rp);
     else

@@ -275,6 +275,11 @@ __device__ __forceinline__ void softmin_tile_ctr(const float* __restrict__ rec,
         bv[4 * v + 2] = t.z;
         bv[4 * v + 3] = t.w;
       }
+      if constexpr (R % 4 == 2) {  // (R = 2: one float2)
+        const float2 t = reinterpret_cast<const float2*>(bias + (j + g) * R)[R / 2 - 1];
+        bv[R - 2] = t.x;
+        bv[R - 1] = t.y;
+      }
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         if (!((PM >> p) & 1)) continue;  // row pair without a needed group (block-sparse plan)
@@ -473,6 +478,8 @@ __global__ void __launch_bounds__(128, MINB) softmin_ctr_kernel(const SoftminArg
       float4* b4 = reinterpret_cast<float4*>(sbias + (tid + 128 * h) * R);
 #pragma unroll
       for (int v = 0; v < R / 4; ++v) b4[v] = make_float4(bb[4 * v], bb[4 * v + 1], bb[4 * v + 2], bb[4 * v + 3]);
+      if constexpr (R % 4 == 2)
+        reinterpret_cast<float2*>(sbias + (tid + 128 * h) * R)[R / 2 - 1] = make_float2(bb[R - 2], bb[R - 1]);
     }
     double tc[KX];
 #pragma unroll
