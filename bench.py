@@ -18,7 +18,16 @@ the step's inputs copied from pinned host memory and the potentials copied
 back inside the timed region. ``--impl reference`` times the CPU oracle
 (oracle/, a numpy/scipy restatement of the reference's ``_softmin``; the
 reference package itself is pure Python and cannot be shipped to the box) on
-all host cores, on bounded row samples of the same workload.
+all host cores, on bounded row samples of the same workload; that arm never
+imports this package (configs.py is loaded by path) so no GPU library is
+mapped into it.
+
+The second half of the BASELINE metric, GW solve time at N=M=2^20, is the
+``solve`` object of the same line (``--no-solve`` skips it): the C4 config
+(10 outer steps x 100 Sinkhorn sweeps at eps = 0.01, the automatic kernel
+path) through the public solver state from host arrays, CUDA events around
+the whole solve, clocks sampled while it runs; beside it the C1 solve on the
+GPU and the CPU oracle's C1 solve on the host cores.
 """
 
 from __future__ import annotations
@@ -52,6 +61,9 @@ def parse():
     p.add_argument("--size", type=int, default=C2["n"], help="override N=M (smoke runs)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-solve", action="store_true", help="skip the GW solve-time block")
+    p.add_argument("--solve-n", type=int, default=1 << 20, help="C4 solve size (N=M)")
+    p.add_argument("--solve-outer", type=int, default=10)
     p.add_argument("--backend", default=None, choices=[None, "nccl", "gloo"],
                    help="collective backend under torchrun (default nccl; gloo only for "
                         "single-GPU functional checks of the multi-rank path)")
@@ -125,6 +137,21 @@ def probe_peaks():
     return peaks
 
 
+def load_configs():
+    """paper_2602_06658_b200/configs.py by path: the synthetic-input generators
+    without importing the package (whose import maps the GPU library)."""
+    import importlib.util
+
+    path = os.path.join(ROOT, "paper_2602_06658_b200", "configs.py")
+    if "_cntgw_configs" in sys.modules:
+        return sys.modules["_cntgw_configs"]
+    spec = importlib.util.spec_from_file_location("_cntgw_configs", path)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["_cntgw_configs"] = mod  # dataclasses resolve their module by name
+    spec.loader.exec_module(mod)
+    return mod
+
+
 # ---------------------------------------------------------------------------
 # CPU oracle timing (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------
@@ -157,35 +184,71 @@ def workload_config(n, m, world):
             "l2": "flushed by a 256 MiB write before every timed step"}
 
 
-def run_reference(args, info):
-    """--impl reference: the CPU oracle on bounded samples of the same workload."""
-    from paper_2602_06658_b200 import configs
+def cpu_c1_solve():
+    """The oracle's C1 solve (reference solvers.py:628-632 restated) on the
+    host: wall seconds, outer steps, inner sweeps, value."""
+    from oracle import cntgw_oracle as O
 
+    configs = load_configs()
+    pc = configs.c1(seed=0)
+    x = pc.x - pc.a @ pc.x
+    y = pc.y - pc.b @ pc.y
+    t0 = time.perf_counter()
+    ref = O.solve_cnt_gw(x, pc.a, y, pc.b, configs.C1_EPS, dict(threshold=1e-5, max_inner=200),
+                         max_outer=20)
+    dt = time.perf_counter() - t0
+    return {"config": "C1 (N=M=1000, eps=0.01, tau=1e-5, <=20 outer)", "seconds": dt,
+            "outer": len(ref["trace"]["objective"]), "inner_iters": list(ref["trace"]["inner_iters"]),
+            "value": float(ref["value"]), "kind": "port",
+            "what": "oracle/cntgw_oracle.py solve_cnt_gw (numpy/scipy restatement of the reference)"}
+
+
+def run_reference(args, info):
+    """--impl reference: the CPU oracle on bounded samples of the same workload.
+
+    A step is one f-update over a sample of rows at full M (the reference's
+    `_softmin` arithmetic); `value` is the sample's pairs / measured seconds
+    and `ms_per_step` the measured seconds of one sampled step — what the
+    driver's clock sees. The time one FULL N x M step would take at that rate
+    is reported separately (`extrapolated_full_step_ms`)."""
     if info.rank != 0:
         return
+    configs = load_configs()
     n = args.size
     inst = configs.c2(seed=C2["seed"], n=n, k=C2["k"])
     threads = os.cpu_count() or 1
-    rates = []
+    secs, pairs = [], []
     sample = None
     for step in range(args.warmup + args.steps):
         rate, sample = cpu_softmin_rate(inst, rows_target_s=2.0, threads=threads)
         if step >= args.warmup:
-            rates.append(rate)
-    value = float(np.mean(rates))
-    ms = 2.0 * n * n / value * 1e3
+            secs.append(sample["seconds"])
+            pairs.append(sample["rows"] * sample["cols"])
+    value = float(sum(pairs) / sum(secs))
     line = {
         "impl": "reference", "metric": "softmin_pairs_per_s", "value": value, "unit": "pairs/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(secs) / len(secs),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded C2 law)",
         "config": workload_config(n, n, args.gpus),
+        "sampled_step": {"rows": sample["rows"], "cols": sample["cols"],
+                         "note": "each timed step is this row sample of the f-update at full M"},
+        "extrapolated_full_step_ms": 2.0 * n * n / value * 1e3,
         "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port",
                          "sample": f"{sample['rows']} rows x {sample['cols']} cols f-update per step "
-                                   "(oracle/cntgw_oracle.py softmin, numpy+scipy logsumexp); "
-                                   "pairs/s of the sample stand for the full N x M step"},
+                                   "(oracle/cntgw_oracle.py softmin, numpy+scipy logsumexp)"},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_solve:
+        c1 = cpu_c1_solve()
+        passes = args.solve_outer * (2 * 100 + 2)
+        line["solve"] = {
+            "c1": c1,
+            "c4_extrapolated_s": passes * float(args.solve_n) ** 2 / value,
+            "c4_note": f"C4 ({args.solve_n}^2, {args.solve_outer} outer x 100 sweeps) at the measured "
+                       "softmin rate; a full-size CPU run is infeasible (SURVEY.md §8d)",
+        }
     print(json.dumps(line), flush=True)
 
 
@@ -330,6 +393,12 @@ def run_b200(args, info):
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "path": "cntgw_prep_cols + cntgw_softmin (C-ABI) with pinned host inputs"}
 
+    chunked = fwd.ws.numel() > 16  # split-column partials => one combine launch per half-update
+    solve = None
+    if not args.no_solve:
+        del fwd, bwd, src, tgt, flush
+        torch.cuda.empty_cache()
+        solve = gw_solve_block(args, info, dev)
     if info.rank != 0:
         return
     peaks = probe_peaks()
@@ -360,7 +429,7 @@ def run_b200(args, info):
                      "peak_source": peaks["source"], "kernel_avg_ms": kern_avg_ms,
                      "pairs_per_launch": nl * m},
         "e2e": e2e,
-        "gpu_launches": args.steps * (2 * 2 + 2 * (1 if fwd.ws.numel() > 16 else 0)),
+        "gpu_launches": args.steps * (2 * 2 + 2 * (1 if chunked else 0)),
         "clocks": clk,
     }
     if info.world == 1 and not args.no_cpu_baseline:
@@ -369,7 +438,92 @@ def run_b200(args, info):
             "value": rate, "unit": "pairs/s", "cores": sample["threads"], "kind": "port",
             "sample": f"{sample['rows']} sampled rows x {sample['cols']} cols f-update "
                       f"({sample['seconds']:.1f} s; oracle/cntgw_oracle.py softmin, numpy+scipy)"}
+    if solve is not None:
+        if info.world == 1 and not args.no_cpu_baseline:
+            solve["c1_cpu_reference"] = cpu_c1_solve()
+        line["solve"] = solve
     print(json.dumps(line), flush=True)
+
+
+def gw_solve_block(args, info, dev):
+    """Second half of the BASELINE metric: GW solve time at N=M=2^20 (C4).
+
+    The C4 config (BASELINE configs[3]: 10 outer x <= 100 sweeps, eps =
+    0.01) through the public solver state (`_CntGwState`, host arrays in,
+    the automatic kernel path), every outer step run — the cold C4 law trips
+    the reference's own 5-increase guard at step 9, so the
+    config's 10 steps are stepped without the stop rule. CUDA events on the
+    current stream bracket the whole solve (state setup included); max over
+    ranks. Also the C1 solve through `solve_cnt_gw` (one CUDA graph)."""
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2602_06658_b200 as P
+    from paper_2602_06658_b200 import configs, solvers
+
+    def measures(pc):
+        dx, dy = pc.x.shape[1], pc.y.shape[1]
+        spec = P.CostSpec("sq_euclidean")
+        return (P.embed_measure(P.DiscreteMeasure(pc.x, pc.a), spec, dim=dx),
+                P.embed_measure(P.DiscreteMeasure(pc.y, pc.b), spec, dim=dy))
+
+    def barrier():
+        if info.world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    def max_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        if info.world > 1:
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    out = {}
+    # C1 through the public entry point (whole solve = one CUDA graph)
+    pc = configs.c1(seed=0)
+    src, tgt = measures(pc)
+    cfg = P.make_config(configs.C1_EPS, threshold=1e-5, max_inner=200, max_outer=20)
+    P.solve_cnt_gw(src, tgt, cfg)  # warm-up: capture path, allocations
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = P.solve_cnt_gw(src, tgt, cfg)
+    e1.record()
+    barrier()
+    out["c1"] = {"config": "C1 (N=M=1000, eps=0.01, tau=1e-5, <=20 outer)",
+                 "seconds": max_ranks(e0.elapsed_time(e1) * 1e-3), "outer": len(res.trace),
+                 "inner_iters": list(res.trace.inner_iters), "value": res.value}
+    # C4 at full size
+    n, outer, inner = args.solve_n, args.solve_outer, 100
+    pc = configs.c4(seed=0, n=n)
+    src, tgt = measures(pc)
+    cfg = P.make_config(configs.C4_EPS, n_inner=inner, max_outer=outer)
+    barrier()
+    with ClockSampler(dev.index) as clocks:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = solvers._CntGwState(src, tgt, cfg)
+        objs, errs = [], []
+        for _ in range(outer):
+            s = st.step()
+            objs.append(s.objective)
+            errs.append(s.marginal_err)
+        e1.record()
+        barrier()
+    secs = max_ranks(e0.elapsed_time(e1) * 1e-3)
+    passes = outer * (2 * inner + 2)  # 2 half-updates per sweep + final tentative + K4 pass
+    out["c4"] = {
+        "config": f"C4 (N=M={n}, d=3, eps=0.01, {outer} outer x {inner} sweeps)",
+        "seconds": secs, "n_gpus": info.world, "objectives": objs, "marginal_errs": errs,
+        "precision_path": {0: "fp32", 1: "fp64 DMMA", 2: "tcgen05 3xTF32",
+                           3: "block-sparse centred fp32 (F32C)"}[int(st.dev.prec)],
+        "nm_pairs_per_s": passes * float(n) * n / secs,
+        "timing": "CUDA events around state setup + all outer steps (host arrays in), max over ranks",
+        "clocks": clocks.summary(),
+    }
+    del st
+    torch.cuda.empty_cache()
+    return out
 
 
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r1_bench_traffic.json")
@@ -390,16 +544,21 @@ def ncu_traffic(tag, n, m):
     return None
 
 
+class _RankInfo:
+    def __init__(self):
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+
+
 def main():
     args = parse()
+    if args.impl == "reference":
+        # rank 0 alone times the CPU oracle; other ranks exit without work.
+        # Nothing from paper_2602_06658_b200 is imported on this arm.
+        run_reference(args, _RankInfo())
+        return
     from paper_2602_06658_b200 import dist
 
-    if args.impl == "reference":
-        # rank 0 alone times the CPU oracle; other ranks exit without work
-        info = dist.DistInfo(rank=int(os.environ.get("RANK", "0")),
-                             world=int(os.environ.get("WORLD_SIZE", "1")))
-        run_reference(args, info)
-        return
     if args.backend == "gloo" and "CNTGW_BENCH_DEVICE" in os.environ:
         import torch
 

@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define CNTGW_ABI_VERSION 3
+#define CNTGW_ABI_VERSION 4
 
 typedef enum cntgw_status {
   CNTGW_OK = 0,
@@ -174,7 +174,9 @@ int cntgw_prep_cols(const cntgw_sweep_state* st, int prec, int kd, int sq_flag, 
  * tiles that cannot hold a term within 2^-64 of any of its rows' maxima
  * (CNTGW_CTR_SKIP=0 disables it); the plan is reused across the sweeps of a
  * loop (st->sweep > 1) while no column record moved by more than its margin
- * (CNTGW_CTR_REUSE=0 replans every call). */
+ * (CNTGW_CTR_REUSE=0 replans every call). The plan is keyed on the operator
+ * (row block and column block pointers, n, m) and on st->lam_d: a call with a
+ * different key, an annealed lam, or a NaN column record replans. */
 int cntgw_locality_codes(const double* x, int64_t n, int d, int64_t ld, double* bbox, int64_t* codes,
                          void* stream);
 size_t cntgw_ctr_rows_bytes(int64_t n, int kd, int sq_flag);
@@ -184,7 +186,11 @@ int cntgw_prep_rows_ctr(int kd, int sq_flag, const double* feat, int64_t ld, con
 int cntgw_prep_cols_ctr(const cntgw_sweep_state* st, int kd, int sq_flag, const double* feat, int64_t ld,
                         const double* sq, const double* pot, const double* log2w, const int64_t* order,
                         int64_t m, void* cols, void* stream);
-/* Scratch bytes the half-update needs for split-column partials. */
+/* Workspace bytes of one half-update: split-column partials and, for
+ * CNTGW_F32C, the block-sparse plan. The F32C part carries state from call to
+ * call (the plan and its key, see above); a caller may share one workspace
+ * between operators (the key forces a replan on every switch) but then pays a
+ * planning pass per call — keep one workspace per (rows, cols) operator. */
 size_t cntgw_softmin_workspace(int prec, int64_t n, int64_t m, int kd, int sq_flag);
 /* out_i = row_add_i - LSE2_j(t_ij)/lam (row_add nullable => 0). If out_max and
  * out_sum are non-null the per-row (max, sum 2^(t-max)) pair is written instead
@@ -200,10 +206,10 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
 int cntgw_lse_finalize(const cntgw_sweep_state* st, int skip_if_done, int prec, const double* mx,
                        const double* sm, const double* row_add, int64_t n, double* out,
                        void* stream);
-/* Dense-cost half-update (DenseCost provider, sinkhorn.py:30-56), fp32 cost
- * n x m row-major (stride ld): out_i = row_add_i - LSE2_j(lam pot_j + log2w_j
- * - lam C_ij)/lam. */
-int cntgw_softmin_dense(const cntgw_sweep_state* st, int skip_if_done, const float* cost,
+/* Dense-cost half-update (DenseCost provider, sinkhorn.py:30-56), fp64 cost
+ * n x m row-major (stride ld), fp64 throughout like the reference:
+ * out_i = row_add_i - LSE2_j(lam pot_j + log2w_j - lam C_ij)/lam. */
+int cntgw_softmin_dense(const cntgw_sweep_state* st, int skip_if_done, const double* cost,
                         int64_t ld, const double* pot, const double* log2w, const double* row_add,
                         int64_t n, int64_t m, double* out, void* stream);
 
@@ -220,6 +226,24 @@ int cntgw_plan_reduce(const cntgw_sweep_state* st, int kd, int e, const double* 
                       int64_t ld_acc, const double* col_s, int64_t n, int64_t m, double* row_mass,
                       double* pi_y, double* pi_s, int64_t* argmax, void* workspace,
                       size_t workspace_bytes, void* stream);
+
+/* K4 for CNTGW_F32C problems: the same per-row outputs (caller order), from
+ * the centred blocks of the f-half-update (ctr_rows from cntgw_prep_rows_ctr,
+ * ctr_cols from cntgw_prep_cols_ctr with the final g) and that half-update's
+ * workspace (plan_ws: its block-sparse plan is checked / rebuilt for the
+ * current records and the pass skips the (row group, column tile) pairs that
+ * cannot hold a term within 2^-64 of the row's maximum — neither the argmax
+ * nor more than m 2^-64 of the row's mass). Exponents are fp64 from the
+ * original row features (row_feat n x kd, row_sq); col_order = the column
+ * locality order (argmax ties break at the lowest original column);
+ * acc_ws: cntgw_plan_reduce_ctr_workspace(m, e) bytes. */
+size_t cntgw_plan_reduce_ctr_workspace(int64_t m, int e);
+int cntgw_plan_reduce_ctr(const cntgw_sweep_state* st, int kd, int sq_flag, int e, const void* ctr_rows,
+                          const void* ctr_cols, const int64_t* col_order, const double* row_feat,
+                          int64_t ld_row, const double* row_sq, const double* f_tilde, const double* log2a,
+                          const double* col_acc, int64_t ld_acc, const double* col_s, int64_t n, int64_t m,
+                          double* row_mass, double* pi_y, double* pi_s, int64_t* argmax, void* plan_ws,
+                          size_t plan_ws_bytes, void* acc_ws, size_t acc_ws_bytes, void* stream);
 
 /* ---- K5/K7: operator, features and objective (solvers.py:219-220, 330-334) */
 /* out_i = op . feat_i for op dout x din (fp64, dout*din <= 4096): fp64 result

@@ -45,7 +45,7 @@ class OuterStateStruct(ctypes.Structure):
 
 
 F32, F64, TF32X3, F32C = 0, 1, 2, 3  # cntgw_precision
-ABI_VERSION = 3  # CNTGW_ABI_VERSION
+ABI_VERSION = 4  # CNTGW_ABI_VERSION
 
 # name -> (restype, argtypes); every symbol include/cntgw_b200.h declares
 SIGNATURES = {
@@ -75,6 +75,10 @@ SIGNATURES = {
     "cntgw_softmin_dense": (c_int, [c_vp, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64,
                                     c_vp, c_vp]),
     "cntgw_plan_reduce_workspace": (c_size_t, [c_i64, c_i64, c_int, c_int]),
+    "cntgw_plan_reduce_ctr_workspace": (c_size_t, [c_i64, c_int]),
+    "cntgw_plan_reduce_ctr": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp,
+                                      c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,
+                                      c_vp, c_vp, c_size_t, c_vp, c_size_t, c_vp]),
     "cntgw_plan_reduce": (c_int, [c_vp, c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
                                   c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
                                   c_size_t, c_vp]),

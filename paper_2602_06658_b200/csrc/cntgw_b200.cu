@@ -11,6 +11,7 @@
 #include "softmin_ctr.cuh"
 #include "softmin_ctr_tc.cuh"
 #include "softmin_dmma.cuh"
+#include "reduce_ctr.cuh"
 #include "softmin_tc.cuh"
 #include "sweep.cuh"
 
@@ -198,7 +199,7 @@ size_t ctr_plan_bytes(const KernelPick& k, int64_t n, int64_t m) {
   const int64_t ctas = (ctr_groups(n) + k.ctr_r - 1) / k.ctr_r;
   const int64_t tl = (m + kColTile - 1) / kColTile;
   return align256(sizeof(float) * ctas * k.ctr_r * tl) + align256(sizeof(uint32_t) * ctas * tl) +
-         align256(sizeof(double) * tl * kColTile) + 256;  // + c at the last plan, replan flag
+         align256(sizeof(double) * tl * kColTile) + 256;  // + c at the last plan, CtrPlanKey
 }
 
 // CNTGW_F32C, kx <= 4, on tcgen05 (softmin_ctr_tc.cuh), opt-in with CNTGW_CTR_TC=1:
@@ -346,7 +347,7 @@ __global__ void prep_cols_kernel(const cntgw_sweep_state* st, int kd, int sq_fla
 }
 
 // ---- dense cost half-update ---------------------------------------------------
-__global__ void softmin_dense_kernel(const cntgw_sweep_state* st, int skip, const float* cost,
+__global__ void softmin_dense_kernel(const cntgw_sweep_state* st, int skip, const double* cost,
                                      int64_t ld, const double* pot, const double* log2w,
                                      const double* row_add, int64_t n, int64_t m, double* out) {
   if (skip_now(st, skip)) return;
@@ -356,9 +357,9 @@ __global__ void softmin_dense_kernel(const cntgw_sweep_state* st, int skip, cons
   const double lam = st->lam_d;
   double mx = -CUDART_INF;
   double sm = 0.0;
-  const float* ci = cost + i * ld;
+  const double* ci = cost + i * ld;
   for (int64_t j = lane; j < m; j += 32) {
-    const double t = lam * (pot[j] - (double)ci[j]) + log2w[j];
+    const double t = lam * (pot[j] - ci[j]) + log2w[j];
     if (t > mx) {
       sm = sm * exp2(mx - t) + 1.0;
       mx = t;
@@ -435,6 +436,52 @@ __global__ void morton_kernel(const double* x, int64_t n, int d3, int64_t ld, co
 }  // namespace
 
 // ================================================================================
+// Block-sparse plan of the centred kernel (ctr_plan_kernel) in `plan_ws`
+// (ctr_plan_bytes): the reuse check (ctr_plan_check_kernel, keyed on the
+// operator and lam), then the planning pass unless the previous plan holds.
+// Returns the needed-tile votes.
+static const uint32_t* ctr_build_plan(const KernelPick& k, const SoftminArgs& a, void* plan_ws, cudaStream_t s) {
+  const int64_t n = a.n, m = a.m;
+  const int64_t ctas = (ctr_groups(n) + k.ctr_r - 1) / k.ctr_r, tl = (m + kColTile - 1) / kColTile;
+  float* rho = static_cast<float*>(plan_ws);
+  uint32_t* need = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(rho) +
+                                               align256(sizeof(float) * ctas * k.ctr_r * tl));
+  double* c_plan = reinterpret_cast<double*>(reinterpret_cast<char*>(need) +
+                                             align256(sizeof(uint32_t) * ctas * tl));
+  CtrPlanKey* key =
+      reinterpret_cast<CtrPlanKey*>(reinterpret_cast<char*>(c_plan) + align256(sizeof(double) * tl * kColTile));
+  const char* e = getenv("CNTGW_CTR_SKIP_T");
+  const double T = e ? atof(e) : 64.0;
+  // plans are reused across sweeps while the column records moved by at
+  // most `budget` log2 units (CNTGW_CTR_REUSE=0: replan every half-update)
+  const double budget = 8.0;
+  const bool reuse = env_int("CNTGW_CTR_REUSE", 1) != 0;
+  const int64_t mp = tl * kColTile;
+  const CtrCols cv = ctr_cols_view(a.col_rec, mp, k.ctr_kx);
+  const int* rp = nullptr;
+  if (reuse) {
+    if (k.ctr_kx == 4)
+      ctr_plan_check_kernel<4><<<1, 1024, 0, s>>>(a.st, cv.rec64, mp, c_plan, key, a.row_feat, a.col_rec, n, m,
+                                                  budget);
+    else
+      ctr_plan_check_kernel<8><<<1, 1024, 0, s>>>(a.st, cv.rec64, mp, c_plan, key, a.row_feat, a.col_rec, n, m,
+                                                  budget);
+    rp = &key->replan;
+  }
+  const double Tp = reuse ? T + 2.0 * budget : T;
+  // one planning block per streaming CTA (S = 1: planning 4 CTAs per block
+  // to share the column reads measured 2.6x slower, 43 vs 17 ms at 2^20)
+  if (k.ctr_kx == 4 && k.ctr_r == 8)
+    ctr_plan_kernel<4, 8, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, Tp, rp);
+  else if (k.ctr_kx == 4 && k.ctr_r == 2)
+    ctr_plan_kernel<4, 2, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, Tp, rp);
+  else if (k.ctr_kx == 4)
+    ctr_plan_kernel<4, 4, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, Tp, rp);
+  else
+    ctr_plan_kernel<8, 4, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, Tp, rp);
+  return need;
+}
+
 extern "C" {
 
 int cntgw_abi_version(void) { return CNTGW_ABI_VERSION; }
@@ -646,43 +693,7 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
     a.part_sum = a.part_max + (size_t)p.nchunks * n;
   }
   cudaStream_t s = as_stream(stream);
-  if (plan_bytes > 0) {  // block-sparse plan of the centred kernel (ctr_plan_kernel)
-    const int64_t ctas = (ctr_groups(n) + k.ctr_r - 1) / k.ctr_r, tl = (m + kColTile - 1) / kColTile;
-    float* rho = reinterpret_cast<float*>(static_cast<char*>(workspace) + part_bytes);
-    uint32_t* need = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(rho) +
-                                                 align256(sizeof(float) * ctas * k.ctr_r * tl));
-    double* c_plan = reinterpret_cast<double*>(reinterpret_cast<char*>(need) +
-                                               align256(sizeof(uint32_t) * ctas * tl));
-    int* replan = reinterpret_cast<int*>(reinterpret_cast<char*>(c_plan) + align256(sizeof(double) * tl * kColTile));
-    const char* e = getenv("CNTGW_CTR_SKIP_T");
-    const double T = e ? atof(e) : 64.0;
-    // plans are reused across sweeps while the column records moved by at
-    // most `budget` log2 units (CNTGW_CTR_REUSE=0: replan every half-update)
-    const double budget = 8.0;
-    const bool reuse = env_int("CNTGW_CTR_REUSE", 1) != 0;
-    const int64_t mp = tl * kColTile;
-    const CtrCols cv = ctr_cols_view(col_rec, mp, k.ctr_kx);
-    const int* rp = nullptr;
-    if (reuse) {
-      if (k.ctr_kx == 4)
-        ctr_plan_check_kernel<4><<<1, 1024, 0, s>>>(st, cv.rec64, mp, c_plan, replan, budget);
-      else
-        ctr_plan_check_kernel<8><<<1, 1024, 0, s>>>(st, cv.rec64, mp, c_plan, replan, budget);
-      rp = replan;
-    }
-    const double Tp = reuse ? T + 2.0 * budget : T;
-    // one planning block per streaming CTA (S = 1: planning 4 CTAs per block
-    // to share the column reads measured 2.6x slower, 43 vs 17 ms at 2^20)
-    if (k.ctr_kx == 4 && k.ctr_r == 8)
-      ctr_plan_kernel<4, 8, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, Tp, rp);
-    else if (k.ctr_kx == 4 && k.ctr_r == 2)
-      ctr_plan_kernel<4, 2, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, Tp, rp);
-    else if (k.ctr_kx == 4)
-      ctr_plan_kernel<4, 4, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, Tp, rp);
-    else
-      ctr_plan_kernel<8, 4, 1><<<(unsigned)ctas, 128, 0, s>>>(a, rho, need, Tp, rp);
-    a.ctr_need = need;
-  }
+  if (plan_bytes > 0) a.ctr_need = ctr_build_plan(k, a, static_cast<char*>(workspace) + part_bytes, s);
   void* args[] = {&a};
   const cudaError_t e =
       cudaLaunchKernel(k.fn, dim3(p.row_tiles, p.nchunks), dim3(k.threads), args, k.smem, s);
@@ -709,7 +720,7 @@ int cntgw_lse_finalize(const cntgw_sweep_state* st, int skip_if_done, int prec, 
   return check_launch("lse_finalize");
 }
 
-int cntgw_softmin_dense(const cntgw_sweep_state* st, int skip_if_done, const float* cost,
+int cntgw_softmin_dense(const cntgw_sweep_state* st, int skip_if_done, const double* cost,
                         int64_t ld, const double* pot, const double* log2w, const double* row_add,
                         int64_t n, int64_t m, double* out, void* stream) {
   if (!st || !cost || !pot || !log2w || !out || n < 1 || m < 1)
@@ -718,6 +729,92 @@ int cntgw_softmin_dense(const cntgw_sweep_state* st, int skip_if_done, const flo
   softmin_dense_kernel<<<(unsigned)((n + warps - 1) / warps), warps * 32, 0, as_stream(stream)>>>(
       st, skip_if_done, cost, ld, pot, log2w, row_add, n, m, out);
   return check_launch("softmin_dense");
+}
+
+/* ---- K4 on the centred path's block-sparse plan (reduce_ctr.cuh) ---- */
+size_t cntgw_plan_reduce_ctr_workspace(int64_t m, int e) {
+  const int ep = e <= 4 ? 4 : (e <= 8 ? 8 : (e <= 16 ? 16 : (e <= 32 ? 32 : (e <= 64 ? 64 : -1))));
+  if (ep < 0 || e < 1) return 0;
+  return (size_t)cntgw_cols_padded(m) * (size_t)((ep + 1 + 1) / 2 * 2) * sizeof(double);
+}
+
+int cntgw_plan_reduce_ctr(const cntgw_sweep_state* st, int kd, int sq_flag, int e, const void* ctr_rows,
+                          const void* ctr_cols, const int64_t* col_order, const double* row_feat,
+                          int64_t ld_row, const double* row_sq, const double* f_tilde, const double* log2a,
+                          const double* col_acc, int64_t ld_acc, const double* col_s, int64_t n, int64_t m,
+                          double* row_mass, double* pi_y, double* pi_s, int64_t* argmax, void* plan_ws,
+                          size_t plan_ws_bytes, void* acc_ws, size_t acc_ws_bytes, void* stream) {
+  if (!st || !ctr_rows || !ctr_cols || !row_feat || !f_tilde || !log2a || !col_acc || !col_s || !row_mass ||
+      !pi_y || !pi_s || !argmax || n < 1 || m < 1 || e < 1 || (sq_flag && !row_sq))
+    return fail(CNTGW_EINVAL, "plan_reduce_ctr: bad arguments");
+  KernelPick k;
+  if (!lookup(CNTGW_F32C, kd, sq_flag, &k))
+    return fail(CNTGW_EINVAL, "plan_reduce_ctr: no centred kernel for kd=%d sq=%d", kd, sq_flag);
+  // the opt-in tcgen05 centred kernel (CNTGW_CTR_TC=1) keeps the kx = 4 block
+  // layout but has no plan: the pass then visits every tile
+  const int kx = k.ctr_kx > 0 ? k.ctr_kx : 4;
+  const int ep = e <= 4 ? 4 : (e <= 8 ? 8 : (e <= 16 ? 16 : (e <= 32 ? 32 : (e <= 64 ? 64 : -1))));
+  if (ep < 0) return fail(CNTGW_EINVAL, "plan_reduce_ctr: unsupported e=%d", e);
+  const size_t acc_need = cntgw_plan_reduce_ctr_workspace(m, e);
+  if (!acc_ws || acc_ws_bytes < acc_need)
+    return fail(CNTGW_ENOSPACE, "plan_reduce_ctr workspace %zu < %zu", acc_ws_bytes, acc_need);
+  const size_t plan_bytes = ctr_plan_bytes(k, n, m);
+  const size_t part_bytes = plan_bytes > 0 ? align256(plan_workspace(plan_softmin(n, m, k), n)) : 0;
+  if (plan_bytes > 0 && (!plan_ws || plan_ws_bytes < part_bytes + plan_bytes))
+    return fail(CNTGW_ENOSPACE, "plan_reduce_ctr: plan workspace %zu < %zu", plan_ws_bytes,
+                part_bytes + plan_bytes);
+  cudaStream_t s = as_stream(stream);
+  SoftminArgs sa{};
+  sa.st = st;
+  sa.row_feat = ctr_rows;
+  sa.col_rec = ctr_cols;
+  sa.n = n;
+  sa.m = m;
+  const uint32_t* need =
+      plan_bytes > 0 ? ctr_build_plan(k, sa, static_cast<char*>(plan_ws) + part_bytes, s) : nullptr;
+  const int64_t mpad = cntgw_cols_padded(m);
+  const int stride = (ep + 1 + 1) / 2 * 2;
+  double* acc = static_cast<double*>(acc_ws);
+  pack_acc_ordered_kernel<<<(unsigned)((mpad + 255) / 256), 256, 0, s>>>(col_acc, ld_acc, e, ep, stride, col_s,
+                                                                          col_order, m, mpad, acc);
+  int rc = check_launch("pack_acc_ordered");
+  if (rc) return rc;
+  PlanReduceCtrArgs a{};
+  a.st = st;
+  const CtrRows rv = ctr_rows_view(ctr_rows, n, kx);
+  a.row_order = rv.order;
+  a.col_order = col_order;
+  a.row_feat = row_feat;
+  a.ld_row = ld_row;
+  a.kd = kd;
+  a.sq = sq_flag ? 1 : 0;
+  a.row_sq = row_sq;
+  a.f_tilde = f_tilde;
+  a.log2a = log2a;
+  a.rec64 = ctr_cols_view(ctr_cols, mpad, kx).rec64;
+  a.acc = acc;
+  a.need = need;
+  a.ctr_r = k.ctr_r > 0 ? k.ctr_r : 1;
+  a.n = n;
+  a.m = m;
+  a.row_mass = row_mass;
+  a.pi_y = pi_y;
+  a.e_real = e;
+  a.pi_s = pi_s;
+  a.argmax = argmax;
+  const unsigned blocks = (unsigned)ctr_groups(n);
+#define PRC(KX_, E_)                                                                    \
+  if (kx == KX_ && ep == E_) {                                                         \
+    auto kern = plan_reduce_ctr_kernel<KX_, E_, 4>;                                    \
+    const size_t smem = CtrReduceSmem<KX_, E_>::kBytes;                                \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    kern<<<blocks, 128, smem, s>>>(a);                                                 \
+    return check_launch("plan_reduce_ctr_kernel");                                     \
+  }
+  PRC(4, 4) PRC(4, 8) PRC(4, 16) PRC(4, 32) PRC(4, 64)
+  PRC(8, 4) PRC(8, 8) PRC(8, 16) PRC(8, 32) PRC(8, 64)
+#undef PRC
+  return fail(CNTGW_EINVAL, "plan_reduce_ctr: unsupported kx=%d e=%d", kx, e);
 }
 
 }  // extern "C"

@@ -595,31 +595,60 @@ __global__ void __launch_bounds__(128, MINB) softmin_ctr_kernel(const SoftminArg
 // term t_ij of a half-update shifts by exactly the change of its column's c_j
 // (log2 units; rows' own potentials do not enter), so a plan made with
 // threshold T + 2 budget stays valid while max_j |c_j - c_j(plan)| <= budget
-// and the features are unchanged (they change only between Sinkhorn loops:
-// the first sweep of a loop always replans). One block compares the current
-// column records with the copy taken at the last plan and sets *replan.
+// and the rest of the records (lam-scaled features) is unchanged. One block
+// compares the current column records with the copy taken at the last plan
+// and sets key->replan. It replans unconditionally on the first sweep of a
+// loop (features change only between loops), whenever lam differs from the
+// plan's (annealed sweeps rescale Zr = -2 lam z, not only c), whenever the
+// operator differs (row/column block pointers and sizes: a workspace shared
+// by two operators never reuses the other's plan), and whenever a column
+// record or its planned copy is NaN.
+struct CtrPlanKey {
+  int32_t replan;
+  int32_t pad_;
+  double lam;
+  const void* rows;
+  const void* cols;
+  int64_t n, m;
+};
+
 template <int KX>
 __global__ void __launch_bounds__(1024) ctr_plan_check_kernel(const cntgw_sweep_state* st, const double* rec64,
-                                                              int64_t mpad, double* c_plan, int* replan,
-                                                              double budget) {
+                                                              int64_t mpad, double* c_plan, CtrPlanKey* key,
+                                                              const void* rows, const void* cols, int64_t n,
+                                                              int64_t m, double budget) {
   __shared__ double red[32];
-  __shared__ int go;
-  const bool first = st == nullptr || st->sweep <= 1;
+  __shared__ int go, nan_seen;
+  const double lam = st ? st->lam_d : 0.0;
+  const bool first = st == nullptr || st->sweep <= 1 || key->lam != lam || key->rows != rows ||
+                     key->cols != cols || key->n != n || key->m != m;
+  if (threadIdx.x == 0) nan_seen = 0;
+  __syncthreads();
   double d = 0.0;
+  bool bad = false;
   if (!first)
     for (int64_t j = threadIdx.x; j < mpad; j += blockDim.x) {
       const double c = rec64[j * (KX + 1) + KX], cp = c_plan[j];
-      d = fmax(d, c == cp ? 0.0 : fabs(c - cp));  // (equal infinities: no change; NaN -> replan below)
+      bad |= (c != c) || (cp != cp);
+      d = fmax(d, c == cp ? 0.0 : fabs(c - cp));  // equal infinities: no change
     }
+  if (bad) nan_seen = 1;  // fmax drops NaN, so it is flagged separately
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = d;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double m = 0.0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) m = fmax(m, red[q]);
-    go = (first || !(m <= budget)) ? 1 : 0;
-    *replan = go;
+    double mx = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) mx = fmax(mx, red[q]);
+    go = (first || nan_seen || !(mx <= budget)) ? 1 : 0;
+    key->replan = go;
+    if (go) {
+      key->lam = lam;
+      key->rows = rows;
+      key->cols = cols;
+      key->n = n;
+      key->m = m;
+    }
   }
   __syncthreads();
   if (go)

@@ -365,7 +365,8 @@ class HalfUpdate:
 
 
 class DenseHalfUpdate:
-    """Half-update over an explicit fp32 cost matrix (DenseCost provider)."""
+    """Half-update over an explicit fp64 cost matrix (DenseCost provider,
+    reference sinkhorn.py:30-56 keeps it in float64)."""
 
     def __init__(self, cost: torch.Tensor, cols_log2w: torch.Tensor):
         self.cost = cost.contiguous()

@@ -70,6 +70,12 @@ class DenseCost:
     def rows(self, i0, i1):
         return self._host()[i0:i1]
 
+    def _rows_dev(self, i0, i1, device):
+        src = self._dev if self._dev is not None else self._m[i0:i1]
+        if self._dev is not None:
+            return src[i0:i1].to(device)
+        return torch.as_tensor(np.ascontiguousarray(src), device=device)
+
     def full(self):
         return self._host()
 
@@ -109,10 +115,13 @@ class SquaredEuclideanCost:
             self._dev = (x, z, (x * x).sum(1), (z * z).sum(1))
         return self._dev
 
-    def rows(self, i0, i1):
+    def _rows_dev(self, i0, i1, device=None):
         x, z, sx, sz = self._device()
         blk = sx[i0:i1, None] + sz[None, :] - 2.0 * (x[i0:i1] @ z.T)
-        return blk.clamp_min_(0.0).cpu().numpy()
+        return blk.clamp_min_(0.0)
+
+    def rows(self, i0, i1):
+        return self._rows_dev(i0, i1).cpu().numpy()
 
     def full(self):
         return self.rows(0, self.shape[0])
@@ -140,10 +149,14 @@ class SeparableLowRankCost:
 
     shape = property(lambda self: (self._u.shape[0], self._v.shape[0]))
 
+    def _rows_dev(self, i0, i1, device=None):
+        if getattr(self, "_dev", None) is None:
+            self._dev = tuple(_on_device(t) for t in (self._u, self._v, self._ra, self._cb))
+        u, v, ra, cb = self._dev
+        return ra[i0:i1, None] + cb[None, :] - 2.0 * (u[i0:i1] @ v.T)
+
     def rows(self, i0, i1):
-        u, v = _on_device(self._u[i0:i1]), _on_device(self._v)
-        blk = _on_device(self._ra[i0:i1])[:, None] + _on_device(self._cb)[None, :] - 2.0 * (u @ v.T)
-        return blk.cpu().numpy()
+        return self._rows_dev(i0, i1).cpu().numpy()
 
     def full(self):
         return self.rows(0, self.shape[0])
@@ -269,10 +282,10 @@ def device_problem(cost, a, b, device) -> DeviceProblem:
             "large to stream densely; use SquaredEuclideanCost or SeparableLowRankCost"
         )
     if getattr(cost, "_dev", None) is not None:
-        c = cost._dev.to(device=device, dtype=torch.float32).contiguous()
+        c = cost._dev.to(device=device, dtype=torch.float64).contiguous()
     else:
         dense = cost.full() if hasattr(cost, "full") else cost.rows(0, n)
-        c = torch.as_tensor(np.ascontiguousarray(dense), dtype=torch.float32, device=device)
+        c = torch.as_tensor(np.ascontiguousarray(dense), dtype=torch.float64, device=device)
     la = torch.log2(engine.to_dev64(a, device))
     lb = torch.log2(engine.to_dev64(b, device))
     fwd = engine.DenseHalfUpdate(c, lb)
@@ -325,7 +338,12 @@ def sinkhorn(a, b, cost, config: SinkhornConfig) -> SinkhornResult:
 
 
 def transport_cost(coupling) -> float:
-    """<C, pi> over the coupling's own cost provider (reference sinkhorn.py:261-266)."""
+    """<C, pi> over the coupling's own cost provider (reference sinkhorn.py:261-266):
+    the fused device passes of plan.py (no host blocks)."""
+    from .plan import plan_sums
+
+    if isinstance(coupling, ImplicitCoupling):
+        return plan_sums(coupling).transport
     return float(sum((blk * coupling.cost.rows(i0, i1)).sum()
                      for i0, i1, blk in coupling.row_blocks()))
 

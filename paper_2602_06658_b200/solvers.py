@@ -34,7 +34,7 @@ import torch
 import torch.distributed as tdist
 
 from . import dist, divergence, engine
-from ._native import F32, F64, LIB, call
+from ._native import F32, F32C, F64, LIB, call
 from .measures import DenseCoupling, ImplicitCoupling
 from .sinkhorn import SinkhornConfig, SquaredEuclideanCost, sinkhorn
 
@@ -215,7 +215,8 @@ class _GwDevice:
         self.pi_y = torch.empty(self.n * self.e, dtype=torch.float64, device=device)
         self.pi_s = torch.empty(self.n, dtype=torch.float64, device=device)
         self.argmax = torch.empty(self.n, dtype=torch.int64, device=device)
-        self.ws_plan = torch.empty(int(LIB.cntgw_plan_reduce_workspace(self.n, self.m, self.kd, self.e)),
+        self.ws_plan = torch.empty(max(int(LIB.cntgw_plan_reduce_workspace(self.n, self.m, self.kd, self.e)),
+                                       int(LIB.cntgw_plan_reduce_ctr_workspace(self.m, self.e))),
                                    dtype=torch.uint8, device=device)
         self.acc = torch.zeros(16 + self.d * self.e + 8, dtype=torch.float64, device=device)
         ows = max(int(LIB.cntgw_outer_reduce_workspace(self.n, self.d, self.e)),
@@ -247,18 +248,43 @@ class _GwDevice:
              side.feat64.data_ptr(), 0, self.kd, _stream())
         side.refresh32()
 
+    def plan_pass(self, f, g):
+        """K4 for the final pair: r, pi Y, pi t and argmax per (local) row.
+
+        On the centred path (CNTGW_F32C) the pass reuses the f-half-update's
+        block-sparse plan (cntgw_plan_reduce_ctr: rows and columns in locality
+        order, tiles that cannot hold a term within 2^-64 of a row's maximum
+        skipped); otherwise it is the dense fp64 pass (cntgw_plan_reduce).
+        CNTGW_K4_SPARSE=0 forces the dense pass."""
+        st = self.loop.state
+        stream = _stream()
+        fwd = self.fwd
+        if self.prec == F32C and os.environ.get("CNTGW_K4_SPARSE", "1") != "0":
+            src = self.src
+            call("cntgw_prep_rows_ctr", fwd.kd, 1, src.feat64.data_ptr(), fwd.kd, src.sq64.data_ptr(),
+                 src.locality().data_ptr(), src.n, fwd.ctr_rows.data_ptr(), stream)
+            fwd.pack(st, g, prec=F32C)
+            call("cntgw_plan_reduce_ctr", st.ptr, fwd.kd, 1, self.e, fwd.ctr_rows.data_ptr(),
+                 fwd.ctr_cols.data_ptr(), self.tgt.locality().data_ptr(), src.feat64.data_ptr(),
+                 fwd.kd, self.sx.data_ptr(), f.data_ptr(), src.log2w.data_ptr(), self.y.data_ptr(),
+                 self.e, self.ty.data_ptr(), self.n, self.m, self.r.data_ptr(), self.pi_y.data_ptr(),
+                 self.pi_s.data_ptr(), self.argmax.data_ptr(), fwd.ws.data_ptr(), fwd.ws.numel(),
+                 self.ws_plan.data_ptr(), self.ws_plan.numel(), stream)
+            return
+        fwd.pack(st, g, prec=F64)
+        call("cntgw_plan_reduce", st.ptr, self.kd, self.e, self.src.feat64.data_ptr(), self.kd,
+             self.sx.data_ptr(), f.data_ptr(), self.src.log2w.data_ptr(), fwd.rec.data_ptr(),
+             self.y.data_ptr(), self.e, self.ty.data_ptr(), self.n, self.m, self.r.data_ptr(),
+             self.pi_y.data_ptr(), self.pi_s.data_ptr(), self.argmax.data_ptr(),
+             self.ws_plan.data_ptr(), self.ws_plan.numel(), stream)
+
     def reductions(self, f, g, skip_g: int):
         """K2 tentative (skipped after a symmetrized threshold break), K4, K7."""
         st = self.loop.state
         if self.comm is None:
             self.bwd(st, f, self.loop.gt, skip=skip_g)
-        self.fwd.pack(st, g, prec=F64)
+        self.plan_pass(f, g)
         stream = _stream()
-        call("cntgw_plan_reduce", st.ptr, self.kd, self.e, self.src.feat64.data_ptr(), self.kd,
-             self.sx.data_ptr(), f.data_ptr(), self.src.log2w.data_ptr(), self.fwd.rec.data_ptr(),
-             self.y.data_ptr(), self.e, self.ty.data_ptr(), self.n, self.m, self.r.data_ptr(),
-             self.pi_y.data_ptr(), self.pi_s.data_ptr(), self.argmax.data_ptr(),
-             self.ws_plan.data_ptr(), self.ws_plan.numel(), stream)
         nrow = 16 + self.d * self.e
         call("cntgw_outer_reduce_rows", self.x.data_ptr(), self.d, self.d, self.pi_y.data_ptr(),
              self.e, self.r.data_ptr(), self.pi_s.data_ptr(), f.data_ptr(), self.sx.data_ptr(),
@@ -320,13 +346,8 @@ class _GwDevice:
         if not sym_break:
             self.loop.tentatives(f, g, need_f=False, need_g=True)
         st = self.loop.state
-        self.fwd.pack(st, g, prec=F64)  # fp64 target records at the final lambda for K4
+        self.plan_pass(f, g)  # K4 at the final lambda
         stream = _stream()
-        call("cntgw_plan_reduce", st.ptr, self.kd, self.e, self.src.feat64.data_ptr(), self.kd,
-             self.sx.data_ptr(), f.data_ptr(), self.src.log2w.data_ptr(), self.fwd.rec.data_ptr(),
-             self.y.data_ptr(), self.e, self.ty.data_ptr(), self.n, self.m, self.r.data_ptr(),
-             self.pi_y.data_ptr(), self.pi_s.data_ptr(), self.argmax.data_ptr(),
-             self.ws_plan.data_ptr(), self.ws_plan.numel(), stream)
         nrow = 16 + self.d * self.e
         call("cntgw_outer_reduce_rows", self.x.data_ptr(), self.d, self.d, self.pi_y.data_ptr(),
              self.e, self.r.data_ptr(), self.pi_s.data_ptr(), f.data_ptr(), self.sx.data_ptr(),
@@ -672,42 +693,25 @@ def _plan_pass(coupling, src, tgt, transpose: bool = False):
     """Fused K4 pass over an ImplicitCoupling on a SquaredEuclideanCost
     (augmented features): returns device (r, pi Y, pi s_y, argmax) — or, with
     ``transpose``, the same pass over pi^T: (c, pi^T X, pi^T s_x, argmax_i),
-    the column-side reductions of divergence._plan_reductions."""
-    cost = coupling.cost
-    if not isinstance(cost, SquaredEuclideanCost):
+    the column-side reductions of divergence._plan_reductions (plan.row_pass)."""
+    from . import plan
+
+    if not isinstance(coupling.cost, SquaredEuclideanCost):
         raise TypeError("fused plan reductions need a SquaredEuclideanCost coupling")
     dev = engine.require_cuda()
-    x, z = cost._x, cost._z
-    f_ref, g_ref = coupling.f, coupling.g
-    a_w, b_w = coupling.source_weights, coupling.target_weights
-    acc, acc_s = np.asarray(tgt.features), _half_sq(tgt)
+    form = plan.feature_form(coupling.cost, dev)
+    f, g, a_w, b_w = plan._coupling_tensors(coupling, dev)
+    f_t, g_t = f - form.row_sep, g - form.col_sep
+    acc, acc_s = tgt.features, _half_sq(tgt)
     if transpose:
-        x, z, f_ref, g_ref, a_w, b_w = z, x, g_ref, f_ref, b_w, a_w
-        acc, acc_s = np.asarray(src.features), _half_sq(src)
-    xf, zf = x[:, :-1], z[:, :-1]
-    kd = engine.padded_kd(max(1, xf.shape[1]))
-    e = acc.shape[1]
-    from .sinkhorn import feature_problem
-
-    srcs, _, fwd, _ = feature_problem(xf, x[:, -1], zf, z[:, -1], a_w, b_w, dev)
-    f = engine.to_dev64(f_ref - (xf * xf).sum(1), dev)
-    g = engine.to_dev64(g_ref - (zf * zf).sum(1), dev)
-    st = engine.SweepState(dev)
-    st.init(coupling.eps_eff)
-    fwd.pack(st, g, prec=F64)
-    n, m = x.shape[0], z.shape[0]
-    r = torch.empty(n, dtype=torch.float64, device=dev)
-    pi_y = torch.empty(n * e, dtype=torch.float64, device=dev)
-    pi_s = torch.empty(n, dtype=torch.float64, device=dev)
-    am = torch.empty(n, dtype=torch.int64, device=dev)
-    ws = torch.empty(int(LIB.cntgw_plan_reduce_workspace(n, m, kd, e)), dtype=torch.uint8, device=dev)
-    y = engine.to_dev64(acc, dev)
-    ty = engine.to_dev64(acc_s, dev)
-    call("cntgw_plan_reduce", st.ptr, kd, e, srcs.feat64.data_ptr(), kd, srcs.sq64.data_ptr(),
-         f.data_ptr(), srcs.log2w.data_ptr(), fwd.rec.data_ptr(), y.data_ptr(), e, ty.data_ptr(),
-         n, m, r.data_ptr(), pi_y.data_ptr(), pi_s.data_ptr(), am.data_ptr(), ws.data_ptr(),
-         ws.numel(), _stream())
-    return r, pi_y.view(n, e), pi_s, am
+        form, f_t, g_t, a_w, b_w = form.transpose(), g_t, f_t, b_w, a_w
+        acc, acc_s = src.features, _half_sq(src)
+    e = np.asarray(acc).shape[1]
+    # K4 accumulates at least as many features as it dots (padded widths)
+    acc_d = engine.to_dev64(acc, dev, max(e, form.kd))
+    r, pi_acc, pi_s, am = plan.row_pass(form, f_t, g_t, a_w, b_w, coupling.eps_eff, acc_d,
+                                        engine.to_dev64(acc_s, dev))
+    return r, pi_acc[:, :e].contiguous(), pi_s, am
 
 
 def gamma_step(coupling, src, tgt) -> np.ndarray:
@@ -728,6 +732,8 @@ def egw_objective(gamma, coupling, src, tgt, eps: float) -> float:
 
     gamma = np.asarray(gamma, dtype=np.float64)
     if isinstance(coupling, ImplicitCoupling):
+        # _cnt_reductions (solvers.py:227-256) as device passes: pi Y and pi s_y
+        # from K4, KL from the potentials identity (plan.plan_sums)
         r, pi_y, pi_s, _ = _plan_pass(coupling, src, tgt)
         x = torch.as_tensor(np.asarray(src.features), device=pi_y.device)
         xt_pi_y = (x.t() @ pi_y).cpu().numpy()

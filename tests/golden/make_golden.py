@@ -175,8 +175,44 @@ def gen_c3_stages(n=400, tau=1e-5, max_outer=10):
                inner_iters=np.concatenate(iters) if iters else np.zeros(0, int),
                stage_lengths=np.array([len(i) for i in iters]))
     if prev is not None:
+        idx, gap = _argmax(prev.coupling)
         out.update(f=prev.coupling.f, g=prev.coupling.g, zbar=prev.coupling.cost._z,
-                   eps_eff=prev.coupling.eps_eff)
+                   xbar=prev.coupling.cost._x, eps_eff=prev.coupling.eps_eff, argmax=idx,
+                   argmax_gap=gap)
+    return out
+
+
+def gen_c1_api():
+    """The building-block API on C1 (SURVEY.md §8b entry points): pi_step at
+    the reference's converged Gamma, gamma_step / egw_objective on its plan,
+    and every plan consumer (marginals, Err, KL, <C, pi>, EOT value) on that
+    plan and on the solve's final coupling."""
+    pc = configs.c1(seed=0)
+    src = _embed(pc.x, pc.a, 3)
+    tgt = _embed(pc.y, pc.b, 3)
+    cfg = cntgw.make_config(configs.C1_EPS, threshold=1e-5, max_inner=200, max_outer=20)
+    res = cntgw.solve_cnt_gw(src, tgt, cfg)
+    gamma = res.gamma
+    inner = cntgw.SinkhornConfig(eps=configs.C1_EPS, threshold=1e-5, max_inner=200)
+    pr = cntgw.pi_step(gamma, src, tgt, configs.C1_EPS, inner)
+    cp = pr.coupling
+    gamma_next = cntgw.gamma_step(cp, src, tgt)
+    out = dict(
+        x_feat=src.features, y_feat=tgt.features, a=src.weights, b=tgt.weights, gamma=gamma,
+        pi_f=cp.f, pi_g=cp.g, pi_iters=pr.iterations, pi_err=pr.marginal_err,
+        pi_converged=pr.converged, pi_eps_eff=cp.eps_eff, pi_xbar=cp.cost._x, pi_zbar=cp.cost._z,
+        gamma_next=gamma_next,
+        obj=cntgw.egw_objective(gamma, cp, src, tgt, configs.C1_EPS),
+        obj_next=cntgw.egw_objective(gamma_next, cp, src, tgt, configs.C1_EPS),
+        pi_kl=cntgw.kl_divergence(cp), pi_me=cntgw.marginal_error(cp),
+        pi_row=cp.row_marginal(), pi_col=cp.col_marginal(),
+        pi_tc=cntgw.transport_cost(cp), pi_eot=cntgw.eot_primal_value(cp),
+    )
+    rc = res.coupling
+    out.update(res_f=rc.f, res_g=rc.g, res_xbar=rc.cost._x, res_zbar=rc.cost._z,
+               res_eps_eff=rc.eps_eff, res_kl=cntgw.kl_divergence(rc),
+               res_me=cntgw.marginal_error(rc), res_tc=cntgw.transport_cost(rc),
+               res_row=rc.row_marginal(), res_col=rc.col_marginal())
     return out
 
 
@@ -426,6 +462,7 @@ GENS = {
     "c4law_solve": lambda: gen_law("C4", 1024, configs.C4_EPS, dict(n_inner=100), 10),
     "c5law_solve": lambda: gen_law("C5", 256, configs.C5_EPS, dict(n_inner=200), 10),
     "c3law_stages": gen_c3_stages,
+    "c1_api": gen_c1_api,
     "c2_subsample": gen_c2_subsample,
     "c2_small": gen_c2_small,
     "sinkhorn_cases": gen_sinkhorn_cases,

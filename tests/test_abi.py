@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol():
 def test_abi_version_and_state_layout():
     from paper_2602_06658_b200 import _native
 
-    assert _native.LIB.cntgw_abi_version() == 3
+    assert _native.LIB.cntgw_abi_version() == _native.ABI_VERSION == 4
     assert _native.LIB.cntgw_sweep_state_size() == ctypes.sizeof(_native.SweepStateStruct)
 
 

@@ -141,12 +141,22 @@ def test_centred_path_cold_locality(env, k, n, m, tc, monkeypatch):
         assert np.percentile(e_c, 99) < 0.75 * np.percentile(e_p, 99)
 
 
-def test_centred_block_sparse_skip(env, monkeypatch):
+# the centred kernel's opt-in variants (csrc/cntgw_b200.cu pick_ctr): row
+# groups per CTA (CNTGW_CTR_R), lazy-rebase group width (CNTGW_CTR_G) and the
+# FMA-pipe exp2 share (CNTGW_CTR_POLY); "default" is R=4, G=4, no polynomial
+CTR_VARIANTS = {"default": {}, "r2": {"CNTGW_CTR_R": "2"}, "r8": {"CNTGW_CTR_R": "8"},
+                "g8": {"CNTGW_CTR_G": "8"}, "poly": {"CNTGW_CTR_POLY": "1"}}
+
+
+@pytest.mark.parametrize("variant", list(CTR_VARIANTS))
+def test_centred_block_sparse_skip(env, variant, monkeypatch):
     """The centred kernel's block-sparse plan (tiles that cannot hold a term
     within 2^-64 of a row's maximum are skipped) on a cold clustered law large
     enough for most tiles to be skipped: equal to the dense sweep to 1e-9 and
-    to the fp64 oracle on sampled rows."""
+    to the fp64 oracle on sampled rows — for every shipped kernel variant."""
     P, engine, S, O, torch, dev = env
+    for key, val in CTR_VARIANTS[variant].items():
+        monkeypatch.setenv(key, val)
     rng = np.random.default_rng(11)
     n = m = 1 << 16
     cx = rng.standard_normal((8, 3)) * 2.0
@@ -296,11 +306,13 @@ def test_low_rank_paths(env, prec, k, n, m):
     assert _rel(got, want) < 1e-5
 
 
-def test_centred_plan_reuse_across_sweeps(env, monkeypatch):
+@pytest.mark.parametrize("anneal", [None, 0.05], ids=["fixed", "annealed"])
+def test_centred_plan_reuse_across_sweeps(env, anneal, monkeypatch):
     """A Sinkhorn loop on the centred path reuses its block-sparse plan across
     sweeps while no column record moved by more than the plan's margin: the
     potentials equal those of replanning every half-update (to 1e-9) and of
-    the dense sweep."""
+    the dense sweep. With sqrt annealing (anneal_from) lam changes every
+    sweep, which rescales the whole record: the plan key forces a replan."""
     P, engine, S, O, torch, dev = env
     rng = np.random.default_rng(21)
     n = m = 1 << 15
@@ -309,7 +321,7 @@ def test_centred_plan_reuse_across_sweeps(env, monkeypatch):
     z = cx[rng.integers(0, 8, m)] + rng.standard_normal((m, 3)) * 0.7
     a, b = np.full(n, 1 / n), np.full(m, 1 / m)
     monkeypatch.setenv("CNTGW_PRECISION", "f32c")
-    cfg = P.SinkhornConfig(eps=2e-3, n_inner=30)
+    cfg = P.SinkhornConfig(eps=2e-3, n_inner=30, anneal_from=anneal)
     out = {}
     for tag, env_vars in (("reuse", {}), ("replan", {"CNTGW_CTR_REUSE": "0"}),
                           ("dense", {"CNTGW_CTR_SKIP": "0"})):
