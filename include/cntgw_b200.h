@@ -271,6 +271,32 @@ size_t cntgw_moments_workspace(int64_t n, int d);
 int cntgw_moments(const double* x, int64_t ldx, int d, const double* w, int64_t n, double* out,
                   void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- row-sharded multi-GPU exchange (dist.py) ---------------
+ * One process per GPU, rows partitioned over ranks. The library talks to NCCL
+ * directly (resolved at run time from libnccl.so.2, the instance torch maps)
+ * so that every collective is enqueued on the caller's stream and a sharded
+ * solve is still one graph-captured launch. cntgw_comm_init is collective:
+ * every rank passes the same unique id (rank 0 creates it with
+ * cntgw_comm_unique_id and broadcasts cntgw_comm_id_bytes() bytes). */
+typedef struct cntgw_comm cntgw_comm;
+int cntgw_comm_available(void);  /* 1 if libnccl.so.2 could be resolved */
+int cntgw_comm_nccl_version(void);
+int cntgw_comm_id_bytes(void);
+int cntgw_comm_unique_id(void* id_out);
+int cntgw_comm_init(cntgw_comm** out, int world, int rank, const void* id);
+int cntgw_comm_destroy(cntgw_comm* comm);
+/* fp64 all-reduce, op 0 = sum, 1 = max; send == recv for in place. */
+int cntgw_comm_allreduce(cntgw_comm* comm, const double* send, double* recv, int64_t count, int op,
+                         void* stream);
+/* s_j <- s_j 2^(m_local_j - m_glob_j), 0 for an empty partial (s_j = 0 or
+ * m_local_j = -inf): the local step of the partial-LSE combine. */
+int cntgw_lse_rescale(const double* m_local, const double* m_glob, double* s, int64_t n, void* stream);
+/* The g-update's exchange step: m_glob = allreduce_max(m_local) (out of
+ * place), rescale, s = allreduce_sum(s); then cntgw_lse_finalize(m_glob, s)
+ * gives every rank the identical full g (no broadcast). */
+int cntgw_comm_combine_lse(cntgw_comm* comm, const double* m_local, double* m_glob, double* s, int64_t n,
+                           void* stream);
+
 /* ---- device-resident outer loop under CUDA graphs ------------------------- */
 int cntgw_outer_state_size(void);
 int cntgw_outer_init(cntgw_outer_state* os, double constant, double eps_outer, double delta_outer,

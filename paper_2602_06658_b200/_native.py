@@ -75,6 +75,15 @@ SIGNATURES = {
     "cntgw_softmin_dense": (c_int, [c_vp, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64,
                                     c_vp, c_vp]),
     "cntgw_plan_reduce_workspace": (c_size_t, [c_i64, c_i64, c_int, c_int]),
+    "cntgw_comm_available": (c_int, []),
+    "cntgw_comm_nccl_version": (c_int, []),
+    "cntgw_comm_id_bytes": (c_int, []),
+    "cntgw_comm_unique_id": (c_int, [c_vp]),
+    "cntgw_comm_init": (c_int, [c_vp, c_int, c_int, c_vp]),
+    "cntgw_comm_destroy": (c_int, [c_vp]),
+    "cntgw_comm_allreduce": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp]),
+    "cntgw_lse_rescale": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "cntgw_comm_combine_lse": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "cntgw_plan_reduce_ctr_workspace": (c_size_t, [c_i64, c_int]),
     "cntgw_plan_reduce_ctr": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp,
                                       c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,

@@ -32,6 +32,35 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^y to fp64 accuracy (< 2 ulp) on the FP64 pipe, for the plan passes (K4)
+// whose outputs are reported in fp64: 0 below 2^-1022, y capped at 64
+// (anything above 2^16 only triggers a rebase),
+// y = n + r with n = rint(y) by the 1.5 * 2^52 trick (n lands in the low
+// mantissa word), |r| <= 1/2, e^(r ln2) by its degree-12 Taylor polynomial
+// (truncation < 2e-16), and 2^n written into the exponent field on the ALU.
+__device__ __forceinline__ double exp2_f64(double y) {
+  const bool under = !(y >= -1022.0);  // (also -inf and NaN: a zero-weight term)
+  y = fmin(fmax(y, -1022.0), 64.0);
+  const double t = y + 6755399441055744.0;  // 1.5 * 2^52
+  const double n = t - 6755399441055744.0;
+  const double r = (y - n) * 0.69314718055994530942;
+  double p = 2.0876756987868099e-09;  // 1/12!
+  p = fma(p, r, 2.5052108385441720e-08);
+  p = fma(p, r, 2.7557319223985893e-07);
+  p = fma(p, r, 2.7557319223985888e-06);
+  p = fma(p, r, 2.4801587301587302e-05);
+  p = fma(p, r, 1.9841269841269841e-04);
+  p = fma(p, r, 1.3888888888888889e-03);
+  p = fma(p, r, 8.3333333333333332e-03);
+  p = fma(p, r, 4.1666666666666664e-02);
+  p = fma(p, r, 1.6666666666666666e-01);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int e = __double2loint(t) + 1023;  // biased exponent of 2^n, in [1, 1087]
+  return under ? 0.0 : p * __hiloint2double(e << 20, 0);
+}
+
 // double -> float on the integer ALU pipe (truncating the mantissa), so the
 // fp64 path does not spend a second XU-pipe op (F2F shares the pipe with
 // MUFU.EX2, measured 16/clk/SM). |v| is clamped below at 2^-126.

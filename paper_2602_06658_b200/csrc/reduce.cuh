@@ -97,13 +97,13 @@ __global__ void __launch_bounds__(128) plan_reduce_kernel(const PlanReduceArgs a
           jbest = (int64_t)t * TILE + j + g;
         }
       }
-      float ev[G], gs = 0.f;
+      double ev[G], gs = 0.0;  // fp64 exponentials: the pass reports fp64 sums
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        ev[g] = ex2(f64_to_f32_alu(mq - q[g]));
+        ev[g] = exp2_f64(mq - q[g]);
         gs += ev[g];
       }
-      if (!(gs <= kRebase)) {
+      if (!(gs <= (double)kRebase)) {
         double qmin = q[0];
 #pragma unroll
         for (int g = 1; g < G; ++g) qmin = fmin(qmin, q[g]);
@@ -116,12 +116,12 @@ __global__ void __launch_bounds__(128) plan_reduce_kernel(const PlanReduceArgs a
           mq = qmin;
         }
 #pragma unroll
-        for (int g = 0; g < G; ++g) ev[g] = ex2(f64_to_f32_alu(mq - q[g]));
+        for (int g = 0; g < G; ++g) ev[g] = exp2_f64(mq - q[g]);
       }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const double* y = acr + (j + g) * A::kStride;
-        const double w = (double)ev[g];
+        const double w = ev[g];
         S += w;
         acc_s = fma(w, y[E], acc_s);
 #pragma unroll

@@ -418,7 +418,9 @@ class SinkhornLoop:
         self.state = SweepState(device)
         self.ft = torch.zeros(self.n, dtype=torch.float64, device=device)
         self.gt = torch.zeros(self.m, dtype=torch.float64, device=device)
-        self.pr = torch.zeros(LIB.cntgw_gap_blocks(self.n), dtype=torch.float64, device=device)
+        # row-gap partials sized for the largest shard (same length on every rank)
+        self.gap_n = comm.gap_rows(self.n) if comm is not None else self.n
+        self.pr = torch.zeros(LIB.cntgw_gap_blocks(self.gap_n), dtype=torch.float64, device=device)
         self.pc = torch.zeros(LIB.cntgw_gap_blocks(self.m), dtype=torch.float64, device=device)
         self._graphs = {}
 
@@ -446,18 +448,15 @@ class SinkhornLoop:
             self._g_update(f, self.gt)
             self._gap(self.a_w, f, self.ft, self.pr)
             self._gap(self.b_w, g, self.gt, self.pc)
-            if self.comm is not None:
-                self.comm.reduce_gap_partials(self)
-            call("cntgw_sweep_finish", st.ptr, self.pr.data_ptr(), self.n, self.pc.data_ptr(),
-                 self.m, _stream())
+            pr, nr = (self.pr, self.n) if self.comm is None else self.comm.reduce_gap_partials(self)
+            call("cntgw_sweep_finish", st.ptr, pr.data_ptr(), nr, self.pc.data_ptr(), self.m, _stream())
             call("cntgw_sweep_apply", st.ptr, f.data_ptr(), self.ft.data_ptr(), self.n, 1, _stream())
             call("cntgw_sweep_apply", st.ptr, g.data_ptr(), self.gt.data_ptr(), self.m, 1, _stream())
         else:
             self.fwd(st, g, self.ft)
             self._gap(self.a_w, f, self.ft, self.pr)
-            if self.comm is not None:
-                self.comm.reduce_gap_partials(self)
-            call("cntgw_sweep_finish", st.ptr, self.pr.data_ptr(), self.n, 0, 0, _stream())
+            pr, nr = (self.pr, self.n) if self.comm is None else self.comm.reduce_gap_partials(self)
+            call("cntgw_sweep_finish", st.ptr, pr.data_ptr(), nr, 0, 0, _stream())
             call("cntgw_sweep_apply", st.ptr, f.data_ptr(), self.ft.data_ptr(), self.n, 0, _stream())
             self._g_update(f, g)
 
@@ -498,6 +497,10 @@ class SinkhornLoop:
             torch.cuda.current_stream().wait_stream(side)
             self._graphs[key] = graph
         graph.replay()
+
+    def tentatives_g(self, f, skip=True):
+        """g-tentative of the current pair into self.gt (row-sharded: exchange)."""
+        self._g_update(f, self.gt, skip=skip)
 
     def tentatives(self, f, g, need_f=True, need_g=True):
         """f/g tentatives of the current pair at the loop's final lambda (no skip)."""

@@ -180,10 +180,20 @@ class _GwDevice:
     def __init__(self, src, tgt, device, info=None):
         self.device = device
         self.info = info if info is not None else dist.DistInfo()
-        self.comm = dist.RowShardComm(self.info) if self.info.enabled else None
         x = np.asarray(src.features, dtype=np.float64)
         y = np.asarray(tgt.features, dtype=np.float64)
         self.n_total = x.shape[0]
+        self.comm = None
+        # CNTGW_FORCE_SHARDED=1 runs the sharded code path at world size 1 (a
+        # single-rank native NCCL communicator): the same captured collectives
+        # as a multi-GPU solve, on one GPU
+        forced = os.environ.get("CNTGW_FORCE_SHARDED", "0") == "1"
+        if self.info.enabled or forced:
+            native = dist.NativeComm(self.info) if (dist.native_comm_wanted() or not self.info.enabled) \
+                else None
+            spans = [dist.shard_range(self.n_total, r, self.info.world) for r in range(self.info.world)]
+            self.comm = dist.RowShardComm(self.info, native=native,
+                                          n_rows_max=max(h - l for l, h in spans))
         self.lo, self.hi = dist.shard_range(self.n_total, self.info.rank, self.info.world)
         x = x[self.lo:self.hi]
         self.n, self.d = x.shape
@@ -210,6 +220,8 @@ class _GwDevice:
         self.fwd = engine.HalfUpdate(self.src, self.tgt, True)
         self.bwd = engine.HalfUpdate(self.tgt, self.src, True)
         self.loop = engine.SinkhornLoop(self.fwd, self.bwd, self.a, self.b, device, comm=self.comm)
+        if self.comm is not None:
+            self.comm.prepare(self.m, self.loop.pr.numel(), device)
         # K4 / K7 buffers
         self.r = torch.empty(self.n, dtype=torch.float64, device=device)
         self.pi_y = torch.empty(self.n * self.e, dtype=torch.float64, device=device)
@@ -281,8 +293,7 @@ class _GwDevice:
     def reductions(self, f, g, skip_g: int):
         """K2 tentative (skipped after a symmetrized threshold break), K4, K7."""
         st = self.loop.state
-        if self.comm is None:
-            self.bwd(st, f, self.loop.gt, skip=skip_g)
+        self.loop.tentatives_g(f, skip=skip_g)
         self.plan_pass(f, g)
         stream = _stream()
         nrow = 16 + self.d * self.e
@@ -290,6 +301,8 @@ class _GwDevice:
              self.e, self.r.data_ptr(), self.pi_s.data_ptr(), f.data_ptr(), self.sx.data_ptr(),
              self.a.data_ptr(), self.n, self.acc.data_ptr(), self.ws_outer.data_ptr(),
              self.ws_outer.numel(), stream)
+        if self.comm is not None:  # row-side sums and Gamma_{t+1} over all shards
+            self.comm.allreduce_(self.acc[:nrow])
         call("cntgw_outer_reduce_cols", st.ptr, g.data_ptr(), self.loop.gt.data_ptr(),
              self.ty.data_ptr(), self.b.data_ptr(), self.m, self.acc[nrow:].data_ptr(),
              self.ws_outer.data_ptr(), self.ws_outer.numel(), stream)
@@ -305,7 +318,7 @@ class _GwDevice:
 
     def gather_rows(self, t: torch.Tensor) -> torch.Tensor:
         """Full-length copy of a row-sharded vector (all ranks)."""
-        if self.comm is None:
+        if self.info.world == 1:
             return t
         sizes = [dist.shard_range(self.n_total, r, self.info.world) for r in range(self.info.world)]
         width = max(h - l for l, h in sizes)
@@ -315,15 +328,42 @@ class _GwDevice:
         tdist.all_gather(parts, buf)
         return torch.cat([p[: h - l] for p, (l, h) in zip(parts, sizes)])
 
-    def choose_precision(self, f, g, eps_min):
+    def choose_precision(self, f, g, eps_min, reachable: bool = False):
+        """Pick the half-update path from the exponent scale of the current
+        operator, or — ``reachable`` — of every operator the solve can reach
+        (the graph-captured solve fixes its path for all outer steps)."""
         fmax = f.abs().max()
         if self.comm is not None:
-            tdist.all_reduce(fmax, op=tdist.ReduceOp.MAX)
+            self.comm.allmax_(fmax)
         pot = float(torch.maximum(fmax, g.abs().max()))
-        scale = engine.exponent_scale(eps_min, self.src.feat64, self.sx, self.tgt.feat64, self.ty, pot)
+        if reachable:
+            scale = self.reachable_scale(eps_min, pot)
+        else:
+            scale = engine.exponent_scale(eps_min, self.src.feat64, self.sx, self.tgt.feat64, self.ty, pot)
         self.prec = engine.choose_precision(
             scale, self.kd, True, ctr_deferred=lambda: self._ctr_deferred(eps_min))
         self.loop.set_precision(self.prec)
+
+    def reachable_scale(self, eps: float, pot_abs: float) -> float:
+        """Upper bound of the exponent scale over every reachable operator.
+
+        Gamma_{t+1} = X^T pi Y with pi >= 0 of marginals (a, b), so by
+        Cauchy-Schwarz ||Gamma||_2 <= ||Gamma||_F <= sqrt(T_x T_y), T = sum
+        w |x|^2; the dot term 2 |<x_i, z_j>| of any step is at most
+        2 sqrt(T_x T_y) max|X| max|Y|, and at a Sinkhorn fixed point the
+        interaction potentials are bounded by the interaction cost, |f~|,
+        |g~| <~ dot + sq."""
+        lam = math.log2(math.e) / eps
+        tx = (self.a * (self.x * self.x).sum(1)).sum().reshape(1)
+        xm = torch.stack([(self.x * self.x).sum(1).max().sqrt(), self.sx.abs().max()])
+        if self.comm is not None:  # every rank must take the same path
+            self.comm.allreduce_(tx)
+            self.comm.allmax_(xm)
+        ty = float((self.b * (self.y * self.y).sum(1)).sum())
+        ym = float((self.y * self.y).sum(1).max().sqrt())
+        dot = 2.0 * math.sqrt(max(float(tx), 0.0) * max(ty, 0.0)) * float(xm[0]) * ym
+        sq = (float(xm[1]) + float(self.ty.abs().max())) ** 2
+        return lam * (max(pot_abs, dot + sq) + dot + sq)
 
     def _ctr_deferred(self, eps_min):
         if float(self.n_total) * float(self.m) < engine.CTR_MIN_PAIRS:
@@ -332,7 +372,7 @@ class _GwDevice:
                 engine.centred_deferred_fraction(eps_min, self.tgt, self.src))
         if self.comm is not None:  # every rank must pick the same path
             t = torch.tensor([s], dtype=torch.float64, device=self.device)
-            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            self.comm.allmax_(t)
             s = float(t)
         return s
 
@@ -342,22 +382,9 @@ class _GwDevice:
         self.set_gamma(gamma)
         self.choose_precision(f, g, loop_cfg.eps)
         stats = self.loop.run(f, g, loop_cfg, use_graph=use_graph)
-        sym_break = stats.broke and loop_cfg.mode == "symmetrized"
-        if not sym_break:
-            self.loop.tentatives(f, g, need_f=False, need_g=True)
-        st = self.loop.state
-        self.plan_pass(f, g)  # K4 at the final lambda
-        stream = _stream()
-        nrow = 16 + self.d * self.e
-        call("cntgw_outer_reduce_rows", self.x.data_ptr(), self.d, self.d, self.pi_y.data_ptr(),
-             self.e, self.r.data_ptr(), self.pi_s.data_ptr(), f.data_ptr(), self.sx.data_ptr(),
-             self.a.data_ptr(), self.n, self.acc.data_ptr(), self.ws_outer.data_ptr(),
-             self.ws_outer.numel(), stream)
-        call("cntgw_outer_reduce_cols", st.ptr, g.data_ptr(), self.loop.gt.data_ptr(),
-             self.ty.data_ptr(), self.b.data_ptr(), self.m, self.acc[nrow:].data_ptr(),
-             self.ws_outer.data_ptr(), self.ws_outer.numel(), stream)
-        if self.comm is not None:  # row-side sums and Gamma_{t+1} over all shards
-            tdist.all_reduce(self.acc[:nrow], op=tdist.ReduceOp.SUM)
+        # g-tentative (skipped on the device after a symmetrized threshold
+        # break, whose tentatives are already the final ones), K4, K7
+        nrow = self.reductions(f, g, skip_g=2)
         acc = self.acc.cpu().numpy()  # the one host read per outer step
         rows, cols = acc[:16], acc[nrow:]
         gamma_next = acc[16:nrow].reshape(self.d, self.e).copy()
@@ -440,7 +467,8 @@ class _CntGwState:
         self.coupling_gamma = None
         self.eps_eff = None
         self.record = []
-        self.use_graph = self.dev.n * self.dev.m <= (1 << 24) and not info.enabled
+        comm = self.dev.comm
+        self.use_graph = self.dev.n * self.dev.m <= (1 << 24) and (comm is None or comm.capturable)
 
     def step(self, inner_budget=None, anneal_from=None) -> _StepStats:
         inner = self.cfg.inner
@@ -510,7 +538,8 @@ class _DeviceSolve:
         self._struct = OuterStateStruct
         # features and precision for the first step, fixed for the captured solve
         dev.set_gamma(state.gamma)
-        dev.choose_precision(state.f, state.g, self.loop_cfg.eps)
+        # one path for the whole captured solve: safe for every reachable Gamma
+        dev.choose_precision(state.f, state.g, self.loop_cfg.eps, reachable=True)
         self.exec = None
 
     def _capture(self):
@@ -650,13 +679,15 @@ def _run_outer(state, cfg: EgwConfig, adaptive: bool = False) -> EgwResult:
 def solve_cnt_gw(src, tgt, cfg: EgwConfig, _warm_potentials=None) -> EgwResult:
     """Feature-space EGW solve (reference solvers.py:628-632).
 
-    On one GPU the whole outer loop runs as a single CUDA graph
-    (``_DeviceSolve``); row-sharded multi-GPU runs and ``record_iterates``
-    use the host-driven loop over the same device kernels. Set
-    CNTGW_DEVICE_LOOP=0 to force the host-driven loop.
+    The whole outer loop runs as a single CUDA graph (``_DeviceSolve``) on
+    one GPU and on every rank of a row-sharded NCCL run (the exchanges are
+    the library's own NCCL collectives, captured in the graph, dist.py);
+    gloo-backed runs and ``record_iterates`` use the host-driven loop over the
+    same device kernels. CNTGW_DEVICE_LOOP=0 forces the host-driven loop.
     """
     state = _CntGwState(src, tgt, cfg, warm_potentials=_warm_potentials)
-    if (state.dev.comm is None and not cfg.record_iterates
+    comm = state.dev.comm
+    if ((comm is None or comm.capturable) and not cfg.record_iterates
             and os.environ.get("CNTGW_DEVICE_LOOP", "1") != "0"):
         return _run_outer_device(state, cfg)
     return _run_outer(state, cfg)

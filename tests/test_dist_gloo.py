@@ -45,6 +45,7 @@ class _Loop:
         self.bwd = op
         self.state = None
         self.pr = pr
+        self.gap_n = 1
 
 
 def _worker(rank, world, port, results):

@@ -13,11 +13,8 @@ Two kinds of checks:
     inputs, within BASELINE's 1e-4 (the plans come from two solvers);
   * reductions only: an ImplicitCoupling built from the REFERENCE's
     potentials, so the device passes (plan.py) are compared with the
-    reference's host block loops on the identical plan. The K4 pass forms
-    every exponent in fp64 but evaluates 2^(small offset) on MUFU.EX2 (fp32,
-    ~1e-7 relative per entry), so plan entries, marginals and the KL carry
-    ~1e-7 relative error: tolerances 2e-6 (marginals, Err) and 1e-7 (KL,
-    <C, pi>, Gamma, objective).
+    reference's host block loops on the identical plan. The K4 pass is fp64
+    throughout (exponents and their 2^x, common.cuh exp2_f64): 1e-10.
 """
 
 import numpy as np
@@ -93,17 +90,17 @@ def test_reductions_on_the_reference_plan(P, which):
     cost = P.SquaredEuclideanCost(gold[pre + "xbar"], gold[pre + "zbar"])
     cp = P.ImplicitCoupling(gold[pre + "f"], gold[pre + "g"], cost, gold["a"], gold["b"],
                             float(gold[pre + "eps_eff"]))
-    assert P.kl_divergence(cp) == pytest.approx(float(gold[pre + "kl"]), rel=1e-7)
-    assert P.transport_cost(cp) == pytest.approx(float(gold[pre + "tc"]), rel=1e-7)
-    assert P.marginal_error(cp) == pytest.approx(float(gold[pre + "me"]), rel=2e-6, abs=1e-12)
-    assert _rel(cp.row_marginal(), gold[pre + "row"]) < 2e-6
-    assert _rel(cp.col_marginal(), gold[pre + "col"]) < 2e-6
+    assert P.kl_divergence(cp) == pytest.approx(float(gold[pre + "kl"]), rel=1e-10)
+    assert P.transport_cost(cp) == pytest.approx(float(gold[pre + "tc"]), rel=1e-10)
+    assert P.marginal_error(cp) == pytest.approx(float(gold[pre + "me"]), rel=1e-9, abs=1e-14)
+    assert _rel(cp.row_marginal(), gold[pre + "row"]) < 1e-10
+    assert _rel(cp.col_marginal(), gold[pre + "col"]) < 1e-10
     if which == "pi":
         src = P.EmbeddedMeasure(gold["x_feat"], gold["a"])
         tgt = P.EmbeddedMeasure(gold["y_feat"], gold["b"])
-        assert _rel(P.gamma_step(cp, src, tgt), gold["gamma_next"]) < 1e-7
+        assert _rel(P.gamma_step(cp, src, tgt), gold["gamma_next"]) < 1e-10
         assert P.egw_objective(gold["gamma"], cp, src, tgt, 0.01) == pytest.approx(
-            float(gold["obj"]), rel=1e-7)
+            float(gold["obj"]), rel=1e-10)
 
 
 def test_densify_blocks_and_marginals_of_a_dense_cost(P):
@@ -147,12 +144,12 @@ def test_low_rank_coupling_reductions(P):
     cp = res.coupling
     ocost = O.LowRank(inst.u, inst.v, inst.row_sep, inst.col_sep)
     row, col = O.marginals(cp.f, cp.g, ocost, a, b, cp.eps_eff)
-    assert _rel(cp.row_marginal(), row) < 2e-6
-    assert _rel(cp.col_marginal(), col) < 2e-6
-    assert P.kl_divergence(cp) == pytest.approx(O.kl(cp.f, cp.g, ocost, a, b, cp.eps_eff), rel=1e-7)
+    assert _rel(cp.row_marginal(), row) < 1e-10
+    assert _rel(cp.col_marginal(), col) < 1e-10
+    assert P.kl_divergence(cp) == pytest.approx(O.kl(cp.f, cp.g, ocost, a, b, cp.eps_eff), rel=1e-9)
     tc = sum(float((blk * ocost.rows(i0, i1)).sum())
              for i0, i1, blk in O.plan_blocks(cp.f, cp.g, ocost, a, b, cp.eps_eff))
-    assert P.transport_cost(cp) == pytest.approx(tc, rel=1e-7)
+    assert P.transport_cost(cp) == pytest.approx(tc, rel=1e-9)
 
 
 def test_large_coupling_consumers_stay_on_device(P):
@@ -166,7 +163,7 @@ def test_large_coupling_consumers_stay_on_device(P):
     pr = P.pi_step(np.zeros((3, 3)), src, tgt, 0.5, P.SinkhornConfig(eps=0.5, n_inner=20))
     cp = pr.coupling
     row, col = cp.row_marginal(), cp.col_marginal()
-    assert row.sum() == pytest.approx(col.sum(), rel=1e-7)  # both are the plan's total mass
+    assert row.sum() == pytest.approx(col.sum(), rel=1e-10)  # both are the plan's total mass
     assert row.sum() == pytest.approx(1.0, abs=1e-2)
     me = float(np.abs(row - cp.source_weights).sum() + np.abs(col - cp.target_weights).sum())
     # the loop's Err comes from its tentatives, the pass's from explicit sums
