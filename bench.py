@@ -288,8 +288,12 @@ def run_b200(args, info):
     f = torch.zeros(nl, dtype=torch.float64, device=dev)  # f0 - a (unused by standard mode)
     g = engine.to_dev64(inst.g.astype(np.float64) - inst.col_sep, dev)
     comm = dist.RowShardComm(info) if info.enabled else None
+    # under NCCL the exchange is the library's own communicator (csrc/comm.cu):
+    # all-reduce MAX, rescale kernel, all-reduce SUM on the compute stream
+    native = dist.NativeComm(info) if info.enabled and dist.native_comm_wanted() else None
     mx = torch.empty(m, dtype=torch.float64, device=dev)
     sm = torch.empty(m, dtype=torch.float64, device=dev)
+    mglob = torch.empty(m, dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     k_ev = []  # (start, end) events around the softmin kernels
@@ -312,8 +316,12 @@ def run_b200(args, info):
         else:  # partial LSE over local rows + all-reduce (dist.py)
             bwd.pack(st, f)
             bwd.stream(st, None, skip=False, out_max=mx, out_sum=sm)
-            dist.combine_partial_lse(mx, sm)
-            bwd.finalize(st, mx, sm, g, skip=False)
+            if native is not None:
+                native.combine_lse(mx, mglob, sm)
+                bwd.finalize(st, mglob, sm, g, skip=False)
+            else:
+                dist.combine_partial_lse(mx, sm)
+                bwd.finalize(st, mx, sm, g, skip=False)
 
     def barrier():
         if info.enabled:

@@ -61,7 +61,8 @@ typedef enum cntgw_precision {
   CNTGW_F32 = 0,
   CNTGW_F64 = 1,
   CNTGW_TF32X3 = 2,
-  CNTGW_F32C = 3
+  CNTGW_F32C = 3,
+  CNTGW_F64S = 4
 } cntgw_precision;
 
 /* Device-resident state of one Sinkhorn loop (sinkhorn.py:191-258 control).
@@ -186,6 +187,22 @@ int cntgw_prep_rows_ctr(int kd, int sq_flag, const double* feat, int64_t ld, con
 int cntgw_prep_cols_ctr(const cntgw_sweep_state* st, int kd, int sq_flag, const double* feat, int64_t ld,
                         const double* sq, const double* pot, const double* log2w, const int64_t* order,
                         int64_t m, void* cols, void* stream);
+/* ---- K1/K2, CNTGW_F64S: fp64 (DMMA) on ordered rows/columns with a measured
+ * block-sparse plan (softmin_f64s.cuh) — cold problems without low-dimensional
+ * locality (C5). Rows are gathered once per operator into a block in a caller
+ * order (a clustering of the points), columns are packed in their order; the
+ * first sweep of a loop (or any sweep whose column records moved by more than
+ * the plan's margin) runs densely and measures, per (row group, column
+ * stage), whether any row holds a term within 2^-80 of its maximum; the
+ * other sweeps walk only those stages. Outputs are in the caller's order;
+ * the workspace (cntgw_softmin_workspace) holds the plan. */
+size_t cntgw_f64s_rows_bytes(int64_t n, int kd);
+int cntgw_prep_rows_f64s(int kd, int sq_flag, const double* feat, int64_t ld, const double* sq,
+                         const int64_t* order, int64_t n, void* rows, void* stream);
+/* cntgw_prep_cols (CNTGW_F64 records) with the columns gathered in `order`. */
+int cntgw_prep_cols_f64s(const cntgw_sweep_state* st, int kd, int sq_flag, const double* feat, int64_t ld,
+                         const double* sq, const double* pot, const double* log2w, const int64_t* order,
+                         int64_t m, void* rec, void* stream);
 /* Workspace bytes of one half-update: split-column partials and, for
  * CNTGW_F32C, the block-sparse plan. The F32C part carries state from call to
  * call (the plan and its key, see above); a caller may share one workspace
@@ -244,6 +261,20 @@ int cntgw_plan_reduce_ctr(const cntgw_sweep_state* st, int kd, int sq_flag, int 
                           const double* col_acc, int64_t ld_acc, const double* col_s, int64_t n, int64_t m,
                           double* row_mass, double* pi_y, double* pi_s, int64_t* argmax, void* plan_ws,
                           size_t plan_ws_bytes, void* acc_ws, size_t acc_ws_bytes, void* stream);
+
+/* K4 for CNTGW_F64S problems: the same per-row outputs (caller order) from
+ * the f-half-update's rows block (cntgw_prep_rows_f64s) and ordered fp64
+ * records of the final g (cntgw_prep_cols_f64s), skipping the (row group,
+ * stage) pairs of that half-update's measured plan (plan_ws = its workspace)
+ * while the plan still holds for these records, every stage otherwise;
+ * col_order = the column order (argmax ties at the lowest original column).
+ * sq_flag must be 1 (the GW cost). acc_ws: cntgw_plan_reduce_ctr_workspace. */
+int cntgw_plan_reduce_f64s(const cntgw_sweep_state* st, int kd, int sq_flag, int e, const void* f64s_rows,
+                           const double* col_rec, const int64_t* col_order, const double* row_feat,
+                           int64_t ld_row, const double* row_sq, const double* f_tilde, const double* log2a,
+                           const double* col_acc, int64_t ld_acc, const double* col_s, int64_t n, int64_t m,
+                           double* row_mass, double* pi_y, double* pi_s, int64_t* argmax, void* plan_ws,
+                           size_t plan_ws_bytes, void* acc_ws, size_t acc_ws_bytes, void* stream);
 
 /* ---- K5/K7: operator, features and objective (solvers.py:219-220, 330-334) */
 /* out_i = op . feat_i for op dout x din (fp64, dout*din <= 4096): fp64 result

@@ -44,7 +44,7 @@ class OuterStateStruct(ctypes.Structure):
     ]
 
 
-F32, F64, TF32X3, F32C = 0, 1, 2, 3  # cntgw_precision
+F32, F64, TF32X3, F32C, F64S = 0, 1, 2, 3, 4  # cntgw_precision
 ABI_VERSION = 4  # CNTGW_ABI_VERSION
 
 # name -> (restype, argtypes); every symbol include/cntgw_b200.h declares
@@ -84,6 +84,13 @@ SIGNATURES = {
     "cntgw_comm_allreduce": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp]),
     "cntgw_lse_rescale": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
     "cntgw_comm_combine_lse": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "cntgw_f64s_rows_bytes": (c_size_t, [c_i64, c_int]),
+    "cntgw_prep_rows_f64s": (c_int, [c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "cntgw_prep_cols_f64s": (c_int, [c_vp, c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,
+                                     c_vp, c_vp]),
+    "cntgw_plan_reduce_f64s": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp,
+                                       c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,
+                                       c_vp, c_vp, c_size_t, c_vp, c_size_t, c_vp]),
     "cntgw_plan_reduce_ctr_workspace": (c_size_t, [c_i64, c_int]),
     "cntgw_plan_reduce_ctr": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp,
                                       c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,

@@ -11,6 +11,7 @@
 #include "softmin_ctr.cuh"
 #include "softmin_ctr_tc.cuh"
 #include "softmin_dmma.cuh"
+#include "softmin_f64s.cuh"
 #include "reduce_ctr.cuh"
 #include "softmin_tc.cuh"
 #include "sweep.cuh"
@@ -98,7 +99,24 @@ struct KernelPick {
   int cta_rows = 0;      // rows per CTA when not 128 * rows
   int ctr_kx = 0;        // CNTGW_F32C FFMA2 kernel: feature width and groups per CTA
   int ctr_r = 0;         //   (block-sparse plan, ctr_plan_kernel)
+  int f64s_tile = 0;     // CNTGW_F64S: column stage of the measured plan (kernel takes F64sArgs)
 };
+
+// CNTGW_F64S: the DMMA kernel's tiling (same choices as pick<F64>) on ordered
+// rows and columns with a measured block-sparse plan (softmin_f64s.cuh).
+template <int KD, int SQ>
+KernelPick pick_f64s() {
+  constexpr int RG = KD >= 64 ? 2 : (KD >= 16 ? 4 : 2), NT = KD >= 16 ? 1 : 4;
+  constexpr int TD = KD >= 64 ? 64 : (KD >= 16 ? 128 : 256), MB = KD >= 16 ? 3 : 4;
+  KernelPick k;
+  k.fn = (void*)softmin_f64s_kernel<KD, SQ, RG, NT, TD, MB>;
+  k.rows = 1;
+  k.cta_rows = 32 * RG;
+  k.smem = (size_t)2 * TD * ColLayout<double, KD, SQ>::kStride * sizeof(double);
+  k.rec_bytes = ColLayout<double, KD, SQ>::kStride * sizeof(double);
+  k.f64s_tile = TD;
+  return k;
+}
 
 template <int PREC, int KD, int SQ>
 KernelPick pick() {
@@ -202,6 +220,27 @@ size_t ctr_plan_bytes(const KernelPick& k, int64_t n, int64_t m) {
          align256(sizeof(double) * tl * kColTile) + 256;  // + c at the last plan, CtrPlanKey
 }
 
+// Measured plan of the CNTGW_F64S kernel: tmin [n][stages] fp32, need
+// [row tiles][stages] bytes, c at the last plan [mpad] fp64, CtrPlanKey.
+struct F64sPlanLayout {
+  size_t tmin, need, cplan, total;
+  int stages;
+  int64_t row_tiles;
+};
+F64sPlanLayout f64s_layout(const KernelPick& k, int64_t n, int64_t m) {
+  F64sPlanLayout l{};
+  if (k.f64s_tile == 0) return l;
+  const int64_t mpad = (m + kColTile - 1) / kColTile * kColTile;
+  l.stages = (int)(mpad / k.f64s_tile);
+  l.row_tiles = (n + k.cta_rows - 1) / k.cta_rows;
+  l.tmin = align256(sizeof(float) * (size_t)n * l.stages);
+  l.need = align256((size_t)l.row_tiles * l.stages);
+  l.cplan = align256(sizeof(double) * (size_t)mpad);
+  l.total = l.tmin + l.need + l.cplan + 256;
+  return l;
+}
+size_t f64s_plan_bytes(const KernelPick& k, int64_t n, int64_t m) { return f64s_layout(k, n, m).total; }
+
 // CNTGW_F32C, kx <= 4, on tcgen05 (softmin_ctr_tc.cuh), opt-in with CNTGW_CTR_TC=1:
 // 11% faster than the FFMA2 kernel at the C4 law but its split-tf32 products
 // and tensor-core accumulation move the 10-step C4 trajectory by up to 5.5e-4
@@ -237,6 +276,14 @@ bool lookup(int prec, int kd, int sq, KernelPick* out) {
       return true;
     }
     if (kx <= 8) { *out = pick_ctr<8>(); return true; }
+    return false;
+  }
+  if (prec == CNTGW_F64S) {
+#define PICK_S(K, Q) \
+  if (kd == K && (sq ? 1 : 0) == Q) { *out = pick_f64s<K, Q>(); return true; }
+    PICK_S(1, 0) PICK_S(1, 1) PICK_S(2, 0) PICK_S(2, 1) PICK_S(3, 0) PICK_S(3, 1) PICK_S(4, 0) PICK_S(4, 1)
+    PICK_S(8, 0) PICK_S(8, 1) PICK_S(16, 0) PICK_S(16, 1) PICK_S(32, 0) PICK_S(32, 1) PICK_S(64, 0) PICK_S(64, 1)
+#undef PICK_S
     return false;
   }
   if (prec == CNTGW_TF32X3) {
@@ -318,14 +365,16 @@ size_t plan_workspace(const Plan& p, int64_t n) {
 template <typename T>
 __global__ void prep_cols_kernel(const cntgw_sweep_state* st, int kd, int sq_flag, int stride,
                                  const T* feat, int64_t ld, const T* sq, const double* pot,
-                                 const double* log2w, int64_t m, int64_t mpad, T* rec) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= mpad) return;
-  T* r = rec + j * stride;
+                                 const double* log2w, int64_t m, int64_t mpad, T* rec,
+                                 const int64_t* order = nullptr) {
+  const int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (jj >= mpad) return;
+  T* r = rec + jj * stride;
+  const int64_t j = jj < m && order ? order[jj] : jj;  // source column (CNTGW_F64S: gathered)
   const bool f64 = sizeof(T) == 8;
   const double lam = f64 ? st->lam_d : (double)st->lam;
   const double sl = f64 ? st->sqrt_lam_d : (double)st->sqrt_lam;
-  if (j < m) {
+  if (jj < m) {
     const T two_lam = (T)(2.0 * lam);
     for (int k = 0; k < kd; ++k) r[k] = -two_lam * feat[j * ld + k];
     double beta = lam * (pot ? pot[j] : 0.0) + log2w[j];
@@ -492,7 +541,7 @@ int cntgw_col_stride(int prec, int kd, int sq) {
   if (!kd_supported(kd)) return fail(CNTGW_EINVAL, "unsupported feature width kd=%d", kd);
   const int raw = kd + (sq ? 1 : 0) + 1;
   if (prec == CNTGW_F32) return (raw + 3) / 4 * 4;
-  if (prec == CNTGW_F64) {
+  if (prec == CNTGW_F64 || prec == CNTGW_F64S) {
     const int vec = (raw + 1) / 2 * 2, k4 = (kd + (sq ? 1 : 0) + 3) / 4 * 4;
     return k4 > vec ? k4 : vec;
   }
@@ -650,7 +699,7 @@ int cntgw_prep_cols_ctr(const cntgw_sweep_state* st, int kd, int sq_flag, const 
 size_t cntgw_softmin_workspace(int prec, int64_t n, int64_t m, int kd, int sq_flag) {
   KernelPick k;
   if (n < 1 || m < 1 || !lookup(prec, kd, sq_flag, &k)) return 0;
-  return align256(plan_workspace(plan_softmin(n, m, k), n)) + ctr_plan_bytes(k, n, m);
+  return align256(plan_workspace(plan_softmin(n, m, k), n)) + ctr_plan_bytes(k, n, m) + f64s_plan_bytes(k, n, m);
 }
 
 int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int kd, int sq_flag,
@@ -685,7 +734,8 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
     const char* e = getenv("CNTGW_CTR_TILE_LIMIT");
     a.ctr_limit = e ? atof(e) : 65536.0;
   }
-  const size_t part_bytes = align256(plan_workspace(p, n)), plan_bytes = ctr_plan_bytes(k, n, m);
+  const size_t part_bytes = align256(plan_workspace(p, n)),
+               plan_bytes = ctr_plan_bytes(k, n, m) + f64s_plan_bytes(k, n, m);
   if (part_bytes + plan_bytes > 0 && (workspace == nullptr || workspace_bytes < part_bytes + plan_bytes))
     return fail(CNTGW_ENOSPACE, "softmin workspace %zu < %zu bytes", workspace_bytes, part_bytes + plan_bytes);
   if (p.nchunks > 1) {
@@ -693,7 +743,49 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
     a.part_sum = a.part_max + (size_t)p.nchunks * n;
   }
   cudaStream_t s = as_stream(stream);
-  if (plan_bytes > 0) a.ctr_need = ctr_build_plan(k, a, static_cast<char*>(workspace) + part_bytes, s);
+  if (k.ctr_kx > 0 && ctr_plan_bytes(k, n, m) > 0)
+    a.ctr_need = ctr_build_plan(k, a, static_cast<char*>(workspace) + part_bytes, s);
+  F64sArgs fs{};
+  F64sPlanLayout fl{};
+  if (k.f64s_tile > 0) {  // CNTGW_F64S: plan check, then the sweep (dense + measure, or sparse)
+    fl = f64s_layout(k, n, m);
+    if (p.chunk_cols / k.f64s_tile > 4096)
+      return fail(CNTGW_EINVAL, "softmin f64s: %lld stages per column chunk (max 4096)",
+                  (long long)(p.chunk_cols / k.f64s_tile));
+    char* base = static_cast<char*>(workspace) + part_bytes;
+    fs.tmin = reinterpret_cast<float*>(base);
+    uint8_t* need_w = reinterpret_cast<uint8_t*>(base + fl.tmin);
+    fs.need = need_w;
+    double* c_plan = reinterpret_cast<double*>(base + fl.tmin + fl.need);
+    CtrPlanKey* key = reinterpret_cast<CtrPlanKey*>(base + fl.tmin + fl.need + fl.cplan);
+    fs.row_order = static_cast<const int64_t*>(row_feat);  // the rows block starts with the order
+    fs.replan = &key->replan;
+    fs.stages = fl.stages;
+    const int64_t mpad = (m + kColTile - 1) / kColTile * kColTile;
+    const int stride = cntgw_col_stride(CNTGW_F64S, kd, sq_flag);
+    // CNTGW_CTR_REUSE=0: a fresh measured plan every call (budget < 0)
+    const double budget = env_int("CNTGW_CTR_REUSE", 1) != 0 ? 8.0 : -1.0;
+    f64s_check_kernel<<<1, 1024, 0, s>>>(st, static_cast<const double*>(col_rec), stride, kd + (sq_flag ? 1 : 0),
+                                         mpad, c_plan, key, row_feat, col_rec, n, m, budget, &key->replan, 1);
+    void* args2[] = {&a, &fs};
+    cudaError_t e2 = cudaLaunchKernel(k.fn, dim3(p.row_tiles, p.nchunks), dim3(k.threads), args2, k.smem, s);
+    if (e2 != cudaSuccess) {
+      cudaGetLastError();
+      return fail(CNTGW_ECUDA, "softmin f64s launch: %s", cudaGetErrorString(e2));
+    }
+    const char* te = getenv("CNTGW_CTR_SKIP_T");
+    const float Tp = (float)((te ? atof(te) : 64.0) + 2.0 * (budget > 0 ? budget : 0.0));
+    f64s_vote_kernel<<<(unsigned)fl.row_tiles, 256, sizeof(float) * k.cta_rows, s>>>(
+        fs.replan, fs.tmin, n, fl.stages, k.cta_rows, Tp, need_w);
+    if (const int rc = check_launch("f64s_vote")) return rc;
+    if (p.nchunks > 1) {
+      const int th = 256;
+      lse_combine_kernel<<<(unsigned)((n + th - 1) / th), th, 0, s>>>(
+          st, skip_if_done, prec, a.part_max, a.part_sum, p.nchunks, n, row_add, out, out_max, out_sum);
+      return check_launch("lse_combine");
+    }
+    return CNTGW_OK;
+  }
   void* args[] = {&a};
   const cudaError_t e =
       cudaLaunchKernel(k.fn, dim3(p.row_tiles, p.nchunks), dim3(k.threads), args, k.smem, s);
@@ -729,6 +821,31 @@ int cntgw_softmin_dense(const cntgw_sweep_state* st, int skip_if_done, const dou
   softmin_dense_kernel<<<(unsigned)((n + warps - 1) / warps), warps * 32, 0, as_stream(stream)>>>(
       st, skip_if_done, cost, ld, pot, log2w, row_add, n, m, out);
   return check_launch("softmin_dense");
+}
+
+/* ---- CNTGW_F64S rows block and ordered column records ---- */
+size_t cntgw_f64s_rows_bytes(int64_t n, int kd) { return n < 1 ? 0 : f64s_rows_bytes(n, kd); }
+
+int cntgw_prep_rows_f64s(int kd, int sq_flag, const double* feat, int64_t ld, const double* sq,
+                         const int64_t* order, int64_t n, void* rows, void* stream) {
+  if (!feat || !rows || n < 1 || !kd_supported(kd) || (sq_flag && !sq))
+    return fail(CNTGW_EINVAL, "prep_rows_f64s: bad arguments");
+  f64s_prep_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(kd, sq_flag ? 1 : 0, feat,
+                                                                                    ld, sq, order, n, rows);
+  return check_launch("prep_rows_f64s");
+}
+
+int cntgw_prep_cols_f64s(const cntgw_sweep_state* st, int kd, int sq_flag, const double* feat, int64_t ld,
+                         const double* sq, const double* pot, const double* log2w, const int64_t* order,
+                         int64_t m, void* rec, void* stream) {
+  if (!st || !feat || !log2w || !rec || m < 1 || (sq_flag && !sq))
+    return fail(CNTGW_EINVAL, "prep_cols_f64s: bad arguments");
+  const int stride = cntgw_col_stride(CNTGW_F64S, kd, sq_flag);
+  if (stride < 0) return stride;
+  const int64_t mpad = cntgw_cols_padded(m);
+  prep_cols_kernel<double><<<(unsigned)((mpad + 255) / 256), 256, 0, as_stream(stream)>>>(
+      st, kd, sq_flag ? 1 : 0, stride, feat, ld, sq, pot, log2w, m, mpad, static_cast<double*>(rec), order);
+  return check_launch("prep_cols_f64s");
 }
 
 /* ---- K4 on the centred path's block-sparse plan (reduce_ctr.cuh) ---- */
@@ -815,6 +932,88 @@ int cntgw_plan_reduce_ctr(const cntgw_sweep_state* st, int kd, int sq_flag, int 
   PRC(8, 4) PRC(8, 8) PRC(8, 16) PRC(8, 32) PRC(8, 64)
 #undef PRC
   return fail(CNTGW_EINVAL, "plan_reduce_ctr: unsupported kx=%d e=%d", kx, e);
+}
+
+/* ---- K4 on the CNTGW_F64S measured plan ---- */
+int cntgw_plan_reduce_f64s(const cntgw_sweep_state* st, int kd, int sq_flag, int e, const void* f64s_rows,
+                           const double* col_rec, const int64_t* col_order, const double* row_feat,
+                           int64_t ld_row, const double* row_sq, const double* f_tilde, const double* log2a,
+                           const double* col_acc, int64_t ld_acc, const double* col_s, int64_t n, int64_t m,
+                           double* row_mass, double* pi_y, double* pi_s, int64_t* argmax, void* plan_ws,
+                           size_t plan_ws_bytes, void* acc_ws, size_t acc_ws_bytes, void* stream) {
+  if (!st || !f64s_rows || !col_rec || !row_feat || !f_tilde || !log2a || !col_acc || !col_s || !row_mass ||
+      !pi_y || !pi_s || !argmax || n < 1 || m < 1 || e < 1 || !sq_flag || !row_sq || !plan_ws)
+    return fail(CNTGW_EINVAL, "plan_reduce_f64s: bad arguments");
+  KernelPick k;
+  if (!lookup(CNTGW_F64S, kd, 1, &k)) return fail(CNTGW_EINVAL, "plan_reduce_f64s: unsupported kd=%d", kd);
+  const int ep = e <= 4 ? 4 : (e <= 8 ? 8 : (e <= 16 ? 16 : (e <= 32 ? 32 : (e <= 64 ? 64 : -1))));
+  if (ep < 0) return fail(CNTGW_EINVAL, "plan_reduce_f64s: unsupported e=%d", e);
+  const size_t acc_need = cntgw_plan_reduce_ctr_workspace(m, e);
+  if (!acc_ws || acc_ws_bytes < acc_need)
+    return fail(CNTGW_ENOSPACE, "plan_reduce_f64s workspace %zu < %zu", acc_ws_bytes, acc_need);
+  const size_t part_bytes = align256(plan_workspace(plan_softmin(n, m, k), n));
+  const F64sPlanLayout fl = f64s_layout(k, n, m);
+  if (plan_ws_bytes < part_bytes + fl.total)
+    return fail(CNTGW_ENOSPACE, "plan_reduce_f64s: plan workspace %zu < %zu", plan_ws_bytes, part_bytes + fl.total);
+  cudaStream_t s = as_stream(stream);
+  char* base = static_cast<char*>(plan_ws) + part_bytes;
+  const uint8_t* need = reinterpret_cast<const uint8_t*>(base + fl.tmin);
+  double* c_plan = reinterpret_cast<double*>(base + fl.tmin + fl.need);
+  CtrPlanKey* key = reinterpret_cast<CtrPlanKey*>(base + fl.tmin + fl.need + fl.cplan);
+  int* stale = &key->pad_;  // this pass's own verdict (the half-update's flag is left alone)
+  const int64_t mpad = cntgw_cols_padded(m);
+  const int stride = cntgw_col_stride(CNTGW_F64S, kd, 1);
+  const double budget = env_int("CNTGW_CTR_REUSE", 1) != 0 ? 8.0 : -1.0;
+  f64s_check_kernel<<<1, 1024, 0, s>>>(st, col_rec, stride, kd + 1, mpad, c_plan, key, f64s_rows, col_rec, n, m,
+                                       budget, stale, 0);
+  if (const int rc = check_launch("f64s_check")) return rc;
+  const int stride_acc = (ep + 1 + 1) / 2 * 2;
+  double* acc = static_cast<double*>(acc_ws);
+  pack_acc_ordered_kernel<<<(unsigned)((mpad + 255) / 256), 256, 0, s>>>(col_acc, ld_acc, e, ep, stride_acc, col_s,
+                                                                          col_order, m, mpad, acc);
+  if (const int rc = check_launch("pack_acc_ordered")) return rc;
+  PlanReduceCtrArgs a{};
+  a.st = st;
+  a.row_order = static_cast<const int64_t*>(f64s_rows);  // the rows block starts with the order
+  a.col_order = col_order;
+  a.row_feat = row_feat;
+  a.ld_row = ld_row;
+  a.kd = kd;
+  a.sq = 1;
+  a.row_sq = row_sq;
+  a.f_tilde = f_tilde;
+  a.log2a = log2a;
+  a.rec64 = col_rec;
+  a.acc = acc;
+  a.need = nullptr;
+  a.ctr_r = 1;
+  a.need8 = need;
+  a.replan = stale;
+  a.grows = k.cta_rows;
+  a.n = n;
+  a.m = m;
+  a.row_mass = row_mass;
+  a.pi_y = pi_y;
+  a.e_real = e;
+  a.pi_s = pi_s;
+  a.argmax = argmax;
+  const unsigned blocks = (unsigned)ctr_groups(n);
+#define PRS(KD_, E_)                                                                                 \
+  if (kd == KD_ && ep == E_) {                                                                       \
+    constexpr int KX = KD_ + 1, STR = ColLayout<double, KD_, 1>::kStride;                           \
+    constexpr int TD = KD_ >= 64 ? 64 : (KD_ >= 16 ? 128 : 256);                                     \
+    auto kern = plan_reduce_ctr_kernel<KX, E_, 4, STR, TD>;                                          \
+    const size_t smem = CtrReduceSmem<STR, E_, TD>::kBytes;                                          \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
+    kern<<<blocks, 128, smem, s>>>(a);                                                               \
+    return check_launch("plan_reduce_f64s_kernel");                                                  \
+  }
+  PRS(1, 4) PRS(2, 4) PRS(3, 4) PRS(4, 4) PRS(1, 8) PRS(2, 8) PRS(3, 8) PRS(4, 8) PRS(8, 8)
+  PRS(1, 16) PRS(2, 16) PRS(3, 16) PRS(4, 16) PRS(8, 16) PRS(16, 16)
+  PRS(1, 32) PRS(2, 32) PRS(3, 32) PRS(4, 32) PRS(8, 32) PRS(16, 32) PRS(32, 32)
+  PRS(1, 64) PRS(2, 64) PRS(3, 64) PRS(4, 64) PRS(8, 64) PRS(16, 64) PRS(32, 64) PRS(64, 64)
+#undef PRS
+  return fail(CNTGW_EINVAL, "plan_reduce_f64s: unsupported kd=%d e=%d", kd, e);
 }
 
 }  // extern "C"

@@ -31,10 +31,13 @@ struct PlanReduceCtrArgs {
   const double* row_sq;
   const double* f_tilde;
   const double* log2a;
-  const double* rec64;  // [mpad][KX+1] fp64 [Zr | c], locality order (ctr column block)
+  const double* rec64;  // [mpad][stride] fp64 [Zr (KX) | c | pad], locality order
   const double* acc;    // [mpad][AccLayout<E>::kStride] [Y | s], locality order
-  const uint32_t* need; // [CTA of R groups][tile] votes, or null (dense)
+  const uint32_t* need; // CNTGW_F32C: [CTA of R groups][256-col tile] votes, or null (dense)
   int ctr_r;
+  const uint8_t* need8; // CNTGW_F64S: [row group of grows rows][stage] bytes, or null
+  const int* replan;    // CNTGW_F64S: the plan is stale for these records (walk every stage)
+  int grows;
   int64_t n, m;
   double* row_mass;
   double* pi_y;
@@ -58,18 +61,22 @@ __global__ void pack_acc_ordered_kernel(const double* y, int64_t ld, int e_real,
   }
 }
 
-template <int KX, int E>
+template <int STRIDE, int E, int TILE = kColTile>
 struct CtrReduceSmem {
-  static constexpr int kRec = kColTile * (KX + 1);            // doubles per stage
-  static constexpr int kAcc = kColTile * AccLayout<E>::kStride;
+  static constexpr int kRec = TILE * STRIDE;                  // doubles per stage
+  static constexpr int kAcc = TILE * AccLayout<E>::kStride;
   static constexpr size_t kBytes = 2 * sizeof(double) * (kRec + kAcc);
 };
 
-// CTA = one 128-row group (locality order), one thread per row, all needed
-// column tiles of that group through a 2-stage bulk-copy ring.
-template <int KX, int E, int G>
+// CTA = 128 rows (locality order), one thread per row, all needed column
+// stages of those rows through a 2-stage bulk-copy ring. KX features [x | s]
+// per row against records [Zr (KX) | c | pad] of STRIDE doubles, stages of
+// TILE columns. The plan is the centred path's (need: words per 256-column
+// tile and CTA of ctr_r groups) or CNTGW_F64S's (need8: bytes per stage and
+// row group of `grows` rows, ignored while *replan).
+template <int KX, int E, int G, int STRIDE = KX + 1, int TILE = kColTile>
 __global__ void __launch_bounds__(128) plan_reduce_ctr_kernel(const PlanReduceCtrArgs a) {
-  using SM = CtrReduceSmem<KX, E>;
+  using SM = CtrReduceSmem<STRIDE, E, TILE>;
   using A = AccLayout<E>;
   extern __shared__ __align__(128) double smem_k4[];
   __shared__ uint64_t bars[2];
@@ -90,12 +97,24 @@ __global__ void __launch_bounds__(128) plan_reduce_ctr_kernel(const PlanReduceCt
   int64_t jbest = INT64_MAX;
 
   const int64_t mpad = (a.m + kColTile - 1) / kColTile * kColTile;
-  const int ntiles = (int)(mpad / kColTile);
+  const int ntiles = (int)(mpad / TILE);
   const uint32_t* need = a.need ? a.need + (grp / a.ctr_r) * ntiles : nullptr;
   const uint32_t vote = 0x01010101u << (grp % a.ctr_r);
+  // F64S: this CTA's 128 rows span 128 / grows plan row groups
+  const bool use8 = a.need8 != nullptr && !(a.replan && *a.replan);
+  const int64_t g8 = grp * kCtrRowGroup / (a.grows > 0 ? a.grows : 1);
+  const int n8 = a.grows > 0 && a.grows < kCtrRowGroup ? kCtrRowGroup / a.grows : 1;
+  const int64_t ng8 = a.grows > 0 ? (a.n + a.grows - 1) / a.grows : 0;
+  auto needed8 = [&](int t) {
+    for (int h = 0; h < n8; ++h)
+      if (g8 + h < ng8 && a.need8[(g8 + h) * ntiles + t]) return true;
+    return false;
+  };
   auto next_needed = [&](int t) {
     if (need)
       while (t < ntiles && !(need[t] & vote)) ++t;
+    else if (use8)
+      while (t < ntiles && !needed8(t)) ++t;
     return t;
   };
   const uint32_t rec_bytes = SM::kRec * sizeof(double), acc_bytes = SM::kAcc * sizeof(double);
@@ -121,16 +140,16 @@ __global__ void __launch_bounds__(128) plan_reduce_ctr_kernel(const PlanReduceCt
     const double* rec = smem_k4 + sb * (SM::kRec + SM::kAcc);
     const double* acr = rec + SM::kRec;
 #pragma unroll 1
-    for (int j = 0; j < kColTile; j += G) {
+    for (int j = 0; j < TILE; j += G) {
       double q[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        const double* c = rec + (j + g) * (KX + 1);
+        const double* c = rec + (j + g) * STRIDE;
         double acc = c[KX];
 #pragma unroll
         for (int k = 0; k < KX; ++k) acc = fma(x[k], c[k], acc);
         q[g] = acc;
-        const int64_t jj = (int64_t)t * kColTile + j + g;
+        const int64_t jj = (int64_t)t * TILE + j + g;
         if (acc <= qbest && acc < kPadQ && jj < a.m) {  // ties: lowest ORIGINAL column (numpy.argmax)
           const int64_t oj = a.col_order ? a.col_order[jj] : jj;
           if (acc < qbest || oj < jbest) {

@@ -413,7 +413,8 @@ static __global__ void lse_combine_kernel(const cntgw_sweep_state* st, int skip,
     out_sum[i] = sm;
   } else {
     const double inv_lam =
-        (prec == CNTGW_F64 || prec == CNTGW_F32C) ? 1.0 / st->lam_d : 1.0 / (double)st->lam;
+        (prec == CNTGW_F64 || prec == CNTGW_F32C || prec == CNTGW_F64S) ? 1.0 / st->lam_d
+                                                                         : 1.0 / (double)st->lam;
     out[i] = (row_add ? row_add[i] : 0.0) - (mx + log2(sm)) * inv_lam;
   }
 }

@@ -592,10 +592,11 @@ __global__ void __launch_bounds__(128, MINB) softmin_ctr_kernel(const SoftminArg
 // so with T = 64 the skipped mass is < m 2^-64 of every row's sum. need:
 // [CTA][tile] 32-bit words, one byte per warp whose bit r votes for group r.
 // Plan reuse across sweeps. Column potentials move every sweep, but every
-// term t_ij of a half-update shifts by exactly the change of its column's c_j
-// (log2 units; rows' own potentials do not enter), so a plan made with
-// threshold T + 2 budget stays valid while max_j |c_j - c_j(plan)| <= budget
-// and the rest of the records (lam-scaled features) is unchanged. One block
+// term t_ij of a half-update shifts by exactly the change d_j of its column's
+// c_j (log2 units; rows' own potentials do not enter) and a row's maximum by
+// the d of some other column, so a plan made with threshold T + 2 budget
+// stays valid while max_j d_j - min_j d_j <= 2 budget and the rest of the
+// records (lam-scaled features) is unchanged. One block
 // compares the current column records with the copy taken at the last plan
 // and sets key->replan. It replans unconditionally on the first sweep of a
 // loop (features change only between loops), whenever lam differs from the
@@ -617,30 +618,45 @@ __global__ void __launch_bounds__(1024) ctr_plan_check_kernel(const cntgw_sweep_
                                                               int64_t mpad, double* c_plan, CtrPlanKey* key,
                                                               const void* rows, const void* cols, int64_t n,
                                                               int64_t m, double budget) {
-  __shared__ double red[32];
+  __shared__ double red[32], red2[32];
   __shared__ int go, nan_seen;
   const double lam = st ? st->lam_d : 0.0;
   const bool first = st == nullptr || st->sweep <= 1 || key->lam != lam || key->rows != rows ||
                      key->cols != cols || key->n != n || key->m != m;
   if (threadIdx.x == 0) nan_seen = 0;
   __syncthreads();
-  double d = 0.0;
+  // validity of the plan: a term skipped with margin T + 2 budget moved by
+  // its column's shift d_j = c_j - c_j(plan), its row's maximum by the shift
+  // of another column, so the plan holds while max_j d_j - min_j d_j <=
+  // 2 budget (a uniform shift of every column changes nothing)
+  double dmx = 0.0, dmn = 0.0;
   bool bad = false;
   if (!first)
-    for (int64_t j = threadIdx.x; j < mpad; j += blockDim.x) {
+    for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
       const double c = rec64[j * (KX + 1) + KX], cp = c_plan[j];
       bad |= (c != c) || (cp != cp);
-      d = fmax(d, c == cp ? 0.0 : fabs(c - cp));  // equal infinities: no change
+      const double d = c == cp ? 0.0 : c - cp;  // equal infinities (zero weight): no change
+      dmx = fmax(dmx, d);
+      dmn = fmin(dmn, d);
     }
-  if (bad) nan_seen = 1;  // fmax drops NaN, so it is flagged separately
+  if (bad) nan_seen = 1;  // fmax/fmin drop NaN, so it is flagged separately
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = d;
+  for (int o = 16; o > 0; o >>= 1) {
+    dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+    dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = dmx;
+    red2[threadIdx.x >> 5] = dmn;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double mx = 0.0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) mx = fmax(mx, red[q]);
-    go = (first || nan_seen || !(mx <= budget)) ? 1 : 0;
+    double mx = 0.0, mn = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+      mx = fmax(mx, red[q]);
+      mn = fmin(mn, red2[q]);
+    }
+    go = (first || nan_seen || !(mx - mn <= 2.0 * budget)) ? 1 : 0;
     key->replan = go;
     if (go) {
       key->lam = lam;

@@ -1,0 +1,290 @@
+// K1/K2, CNTGW_F64S: the fp64 (DMMA) half-update on locality-ordered rows
+// and columns with a MEASURED block-sparse plan — the path of cold problems
+// whose points have no low-dimensional locality to centre on (C5: 64/32-dim
+// features, |exponent| ~ 1e6 log2 units), where the geometric tile bounds of
+// the centred path (softmin_ctr.cuh) are ~1e6 log2 units wide and skip
+// nothing.
+//
+// Same arithmetic as softmin_dmma_kernel (fp64 q_ij = -beta_j + <[x|s]_i,
+// c_j> on mma.sync.m8n8k4.f64, lazily rebased MUFU.EX2 sums). Rows are
+// gathered into a block in the caller-supplied order (cntgw_prep_rows_f64s)
+// and the results scattered back; column records are packed in the column
+// order (cntgw_prep_cols_f64s). A plan is a per-(CTA row group, column
+// stage) mask measured, not bounded:
+//   * replan sweep (the first sweep of a loop, a new operator or lam, or
+//     column records whose shifts since the plan spread over more than
+//     2 budget log2 units, f64s_check_kernel): the kernel walks every stage — the sweep's
+//     outputs are exact — and also writes each row's minimum q over each
+//     stage (tmin, fp32 rounded down); f64s_vote_kernel then marks a stage
+//     needed by a row group when one of its rows has a term within
+//     T + 2 budget log2 units of the row's maximum (T = 64);
+//   * other sweeps walk only the needed stages (their compacted list is
+//     built in shared memory, so the bulk-copy ring stays dense).
+// A term skipped under a plan made with threshold T + 2 budget stays below
+// 2^-T of its row's maximum while max_j d_j - min_j d_j <= 2 budget, d_j the
+// change of column j's record constant -beta_j since the plan (every term of
+// column j shifts by exactly d_j, the row's maximum by the d of some other
+// column), so the skipped mass is < m 2^-64 of every row's sum. On the C5
+// law 4-8% of the (row group, stage) pairs are needed (tools/c5_sparsity.py).
+#pragma once
+
+#include "common.cuh"
+#include "softmin.cuh"
+#include "softmin_ctr.cuh"
+#include "softmin_dmma.cuh"
+
+namespace cntgw {
+
+struct F64sArgs {
+  const int64_t* row_order;  // ordered position -> caller row (rows block)
+  const int* replan;         // device flag from f64s_check_kernel
+  const uint8_t* need;       // [row groups][stages] (row group = one CTA's rows)
+  float* tmin;               // [n][stages] min q per row and stage (replan sweeps)
+  int stages;                // mpad / TD
+};
+
+// Rows block: order [n] int64 | features [n][kd] fp64 | sq [n] fp64.
+__host__ __device__ inline size_t f64s_rows_bytes(int64_t n, int kd) {
+  return align256(sizeof(int64_t) * n) + align256(sizeof(double) * n * kd) + align256(sizeof(double) * n);
+}
+
+__global__ void f64s_prep_rows_kernel(int kd, int sq_flag, const double* feat, int64_t ld, const double* sq,
+                                      const int64_t* order, int64_t n, void* block) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  char* b = static_cast<char*>(block);
+  int64_t* ord = reinterpret_cast<int64_t*>(b);
+  double* f = reinterpret_cast<double*>(b + align256(sizeof(int64_t) * n));
+  double* s = reinterpret_cast<double*>(b + align256(sizeof(int64_t) * n) + align256(sizeof(double) * n * kd));
+  const int64_t src = order ? order[i] : i;
+  ord[i] = src;
+  for (int k = 0; k < kd; ++k) f[i * kd + k] = feat[src * ld + k];
+  s[i] = sq_flag ? sq[src] : 0.0;
+}
+
+// Plan reuse check for the fp64 records: the column constant -beta_j sits at
+// `off` in records of `stride` doubles (same rules as ctr_plan_check_kernel).
+__global__ void __launch_bounds__(1024) f64s_check_kernel(const cntgw_sweep_state* st, const double* rec,
+                                                          int stride, int off, int64_t mpad, double* c_plan,
+                                                          CtrPlanKey* key, const void* rows, const void* cols,
+                                                          int64_t n, int64_t m, double budget,
+                                                          int* flag_out, int commit) {
+  __shared__ double red[32], red2[32];
+  __shared__ int go, nan_seen;
+  const double lam = st ? st->lam_d : 0.0;
+  const bool first = st == nullptr || st->sweep <= 1 || key->lam != lam || key->rows != rows ||
+                     key->cols != cols || key->n != n || key->m != m;
+  if (threadIdx.x == 0) nan_seen = 0;
+  __syncthreads();
+  // validity of the plan: a term skipped with margin T + 2 budget moved by
+  // its column's shift d_j = c_j - c_j(plan), its row's maximum by the shift
+  // of another column, so the plan holds while max_j d_j - min_j d_j <=
+  // 2 budget (a uniform shift of every column changes nothing)
+  double dmx = 0.0, dmn = 0.0;
+  bool bad = false;
+  if (!first)
+    for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
+      const double c = rec[j * stride + off], cp = c_plan[j];
+      bad |= (c != c) || (cp != cp);
+      const double d = c == cp ? 0.0 : c - cp;  // equal infinities (zero weight): no change
+      dmx = fmax(dmx, d);
+      dmn = fmin(dmn, d);
+    }
+  if (bad) nan_seen = 1;  // fmax/fmin drop NaN, so it is flagged separately
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+    dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = dmx;
+    red2[threadIdx.x >> 5] = dmn;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mx = 0.0, mn = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+      mx = fmax(mx, red[q]);
+      mn = fmin(mn, red2[q]);
+    }
+    go = (first || nan_seen || !(mx - mn <= 2.0 * budget)) ? 1 : 0;
+    *flag_out = go;
+    if (go && commit) {
+      key->lam = lam;
+      key->rows = rows;
+      key->cols = cols;
+      key->n = n;
+      key->m = m;
+    }
+  }
+  __syncthreads();
+  // commit = 0: a consumer of the plan (K4) only asks whether it still holds
+  if (go && commit)
+    for (int64_t j = threadIdx.x; j < mpad; j += blockDim.x) c_plan[j] = rec[j * stride + off];
+}
+
+// One block per row group of `grows` rows: each row's minimum over the stage
+// minima (its maximum term), then per stage an OR over the group's rows of
+// "holds a term within Tp of the row maximum" (NaN counts as needed).
+__global__ void __launch_bounds__(256) f64s_vote_kernel(const int* replan, const float* tmin, int64_t n,
+                                                        int stages, int grows, float Tp, uint8_t* need) {
+  if (!*replan) return;
+  extern __shared__ float rowmin[];  // [grows]
+  const int64_t r0 = (int64_t)blockIdx.x * grows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int r = warp; r < grows; r += nw) {
+    float mn = CUDART_INF_F;
+    if (r0 + r < n)
+      for (int t = lane; t < stages; t += 32) mn = fminf(mn, tmin[(r0 + r) * stages + t]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (lane == 0) rowmin[r] = mn;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < stages; t += blockDim.x) {
+    uint8_t v = 0;
+    for (int r = 0; r < grows && r0 + r < n && !v; ++r) {
+      const float q = tmin[(r0 + r) * stages + t], mn = rowmin[r];
+      // tmin and rowmin are rounded down; the allowance covers the fp32
+      // rounding of the sum (NaN keeps the stage)
+      v = !(q > mn + Tp + fabsf(mn) * 0x1p-20f) ? 1 : 0;
+    }
+    need[(int64_t)blockIdx.x * stages + t] = v;
+  }
+}
+
+template <int KD, int SQ, int RG, int NT, int TILE, int MINB, int NS = 2>
+__global__ void __launch_bounds__(128, MINB) softmin_f64s_kernel(const SoftminArgs a, const F64sArgs p) {
+  using L = ColLayout<double, KD, SQ>;
+  constexpr int KS = (KD + SQ + 3) / 4;
+  static_assert(4 * KS <= L::kStride, "column record must cover the padded k4 steps");
+  constexpr int kStage = TILE * L::kStride;
+  constexpr int kMaxList = 4096;  // stages per chunk held in the compacted list
+  extern __shared__ __align__(128) double smem_d[];
+  __shared__ uint64_t full_bar[NS], empty_bar[NS];
+  __shared__ int16_t list[kMaxList];
+  __shared__ int nlist;
+  if (skip_now(a.st, a.skip)) return;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lr = lane >> 2, lk = lane & 3;
+  const int chunk = blockIdx.y;
+  const int64_t wrow = (int64_t)blockIdx.x * (32 * RG) + warp * (8 * RG);
+  const char* rb = static_cast<const char*>(a.row_feat);
+  const double* rf = reinterpret_cast<const double*>(rb + align256(sizeof(int64_t) * a.n));
+  const double* rs = reinterpret_cast<const double*>(rb + align256(sizeof(int64_t) * a.n) +
+                                                     align256(sizeof(double) * a.n * KD));
+  const bool replan = *p.replan != 0;
+
+  double afr[RG][KS];
+  double mq[RG], S[RG];
+#pragma unroll
+  for (int rg = 0; rg < RG; ++rg) {
+    const int64_t i = wrow + 8 * rg + lr;
+    const bool ok = i < a.n;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = 4 * ks + lk;
+      double v = 0.0;
+      if (k < KD) v = ok ? rf[i * KD + k] : 0.0;
+      else if (SQ && k == KD) v = ok ? rs[i] : 0.0;
+      afr[rg][ks] = v;
+    }
+    mq[rg] = kStartQ;
+    S[rg] = 0.0;
+  }
+
+  const int64_t c0 = (int64_t)chunk * a.chunk_cols;
+  const int64_t mpad = (a.m + kColTile - 1) / kColTile * kColTile;
+  const int ntiles = (int)((min(c0 + a.chunk_cols, mpad) - c0) / TILE);
+  const int t0 = (int)(c0 / TILE);  // global stage index of the chunk's first stage
+  // compacted list of the stages this CTA walks (all of them on a replan sweep)
+  if (threadIdx.x == 0) nlist = 0;
+  __syncthreads();
+  {
+    const uint8_t* nd = p.need + (int64_t)blockIdx.x * p.stages + t0;
+    for (int base = 0; base < ntiles; base += blockDim.x) {
+      const int t = base + threadIdx.x;
+      const bool take = t < ntiles && (replan || nd[t]);
+      const unsigned ball = __ballot_sync(0xffffffffu, take);
+      // warp-ordered append: keep the stages in increasing order
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        if (warp == w && lane == 0 && ball) {
+          int pos = nlist;
+          for (unsigned b = ball; b; b &= b - 1) list[pos++] = (int16_t)(base + 32 * w + __ffs(b) - 1);
+          nlist = pos;
+        }
+        __syncthreads();
+      }
+    }
+  }
+  const int nt = nlist;
+  const uint32_t bytes = kStage * sizeof(double);
+  const double* src = static_cast<const double*>(a.col_rec) + c0 * L::kStride;
+  StageRing<NS> ring{full_bar, empty_bar};
+  ring.init(4);
+  if (threadIdx.x == 0)
+    for (int st = 0; st < NS && st < nt; ++st)
+      ring.load(smem_d + st * kStage, src + (int64_t)list[st] * kStage, bytes, st);
+  for (int k = 0; k < nt; ++k) {
+    if (threadIdx.x == 0) {
+      const int r = ring.refill_slot(k, nt);
+      if (r >= 0) ring.load(smem_d + (r % NS) * kStage, src + (int64_t)list[r] * kStage, bytes, r);
+    }
+    ring.wait_full(k);
+    const double* tile = smem_d + (k % NS) * kStage;
+    float T[RG];
+    double tm[RG];
+#pragma unroll
+    for (int rg = 0; rg < RG; ++rg) {
+      T[rg] = 0.f;
+      tm[rg] = CUDART_INF;
+    }
+#pragma unroll 1
+    for (int ct = 0; ct < TILE; ct += 8 * NT) {
+      double q[RG][NT][2];
+      dmma_scores<KD, SQ, RG, NT, KS>(tile, ct, lr, lk, afr, q);
+      if (replan) {
+#pragma unroll
+        for (int rg = 0; rg < RG; ++rg)
+#pragma unroll
+          for (int u = 0; u < NT; ++u) tm[rg] = fmin(tm[rg], fmin(q[rg][u][0], q[rg][u][1]));
+      }
+      dmma_consume<RG, NT>(q, mq, S, T);
+    }
+#pragma unroll
+    for (int rg = 0; rg < RG; ++rg) S[rg] += f32_to_f64_alu(T[rg]);
+    if (replan) {  // the rows' minimum q over this stage (quad = the row's 4 lanes)
+#pragma unroll
+      for (int rg = 0; rg < RG; ++rg) {
+        double v = tm[rg];
+        v = fmin(v, __shfl_xor_sync(0xffffffffu, v, 1));
+        v = fmin(v, __shfl_xor_sync(0xffffffffu, v, 2));
+        const int64_t i = wrow + 8 * rg + lr;
+        if (lk == 0 && i < a.n) p.tmin[i * p.stages + t0 + list[k]] = __double2float_rd(v);
+      }
+    }
+    ring.release(k);
+  }
+
+  const double lam = a.st->lam_d, inv_lam = 1.0 / lam;
+#pragma unroll
+  for (int rg = 0; rg < RG; ++rg) {
+    double m = -mq[rg], s = S[rg];
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      const double mm = fmax(m, m2);
+      s = (s > 0.0 ? s * exp2(m - mm) : 0.0) + (s2 > 0.0 ? s2 * exp2(m2 - mm) : 0.0);
+      m = mm;
+    }
+    const int64_t i = wrow + 8 * rg + lr;
+    if (lk == 0 && i < a.n) {
+      const double si = SQ ? rs[i] : 0.0;
+      softmin_store(a, chunk, p.row_order[i], m - (SQ ? lam * si * si : 0.0), s, inv_lam);
+    }
+  }
+}
+
+}  // namespace cntgw

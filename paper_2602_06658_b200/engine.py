@@ -29,7 +29,7 @@ import numpy as np
 import torch
 
 from . import _native
-from ._native import F32, F32C, F64, LIB, TF32X3, SweepStateStruct, call
+from ._native import F32, F32C, F64, F64S, LIB, TF32X3, SweepStateStruct, call
 
 SUPPORTED_KD = (1, 2, 3, 4, 8, 16, 32, 64)
 # fp32 exponent assembly is used while lam * (term magnitudes) stays below this
@@ -133,6 +133,46 @@ def locality_order(coords: torch.Tensor) -> torch.Tensor:
     return torch.sort(codes, stable=True).indices
 
 
+def cluster_order(points: torch.Tensor, k: int = 64, sweeps: int = 8, seed: int = 0) -> torch.Tensor:
+    """Permutation grouping high-dimensional points by a k-means clustering
+    (CNTGW_F64S row groups / column stages): k seeded centres, `sweeps`
+    Lloyd iterations (streamed assignment ``cntgw_km_assign``; centres as a
+    one-hot fp64 GEMM, deterministic), then points sorted by (cluster, Morton
+    code of their first coordinates)."""
+    x = points.to(torch.float64).contiguous()
+    n, d = x.shape
+    k = max(1, min(k, n))
+    gen = torch.Generator(device="cpu").manual_seed(seed)
+    pick = torch.randperm(n, generator=gen)[:k].to(x.device)
+    centers = x[pick].contiguous()
+    assign = torch.empty(n, dtype=torch.int64, device=x.device)
+    own = torch.empty(n, dtype=torch.float64, device=x.device)
+    for _ in range(sweeps):
+        call("cntgw_km_assign", x.data_ptr(), n, d, centers.data_ptr(), k, assign.data_ptr(),
+             own.data_ptr(), _stream())
+        onehot = torch.nn.functional.one_hot(assign, k).to(torch.float64)
+        counts = onehot.sum(0)
+        sums = onehot.t() @ x
+        keep = counts > 0
+        centers = torch.where(keep[:, None], sums / counts.clamp_min(1.0)[:, None], centers).contiguous()
+    call("cntgw_km_assign", x.data_ptr(), n, d, centers.data_ptr(), k, assign.data_ptr(),
+         own.data_ptr(), _stream())
+    fine = locality_order(x[:, : min(d, 3)])
+    rank = torch.empty_like(fine)
+    rank[fine] = torch.arange(n, device=x.device)
+    return torch.sort(assign * n + rank, stable=True).indices
+
+
+def side_order(feat: torch.Tensor, sq: torch.Tensor | None) -> torch.Tensor:
+    """Locality order of a point cloud: Morton codes when the points are
+    low-dimensional (the centred path's tiles), a k-means cluster order above
+    (the measured-plan path's row groups and column stages)."""
+    real = int((feat.abs().amax(0) > 0).sum()) if feat.numel() else 0
+    if real <= 3 or feat.shape[1] not in (4, 8, 16, 32, 64):
+        return locality_order(feat if sq is None else torch.cat([feat, sq[:, None]], 1))
+    return cluster_order(feat)
+
+
 def _tile_radii(pts: torch.Tensor, order: torch.Tensor, tile: int) -> torch.Tensor:
     """max |p - mean| of each consecutive `tile`-point group in `order`."""
     p = pts[order]
@@ -189,15 +229,25 @@ def tc_supported(kd: int, sq: bool) -> bool:
     return kd in (8, 16) and not sq
 
 
-def choose_precision(scale: float, kd: int = 0, sq: bool = True, ctr_deferred=None) -> int:
+# CNTGW_F64S (fp64 with a measured block-sparse plan) for cold problems the
+# centred path cannot take, from this many pairs per half-update (below it a
+# dense fp64 sweep takes milliseconds and the plan does not pay off)
+F64S_MIN_PAIRS = float(os.environ.get("CNTGW_F64S_MIN_PAIRS", 2.0 ** 34))
+
+
+def choose_precision(scale: float, kd: int = 0, sq: bool = True, ctr_deferred=None,
+                     pairs: float = 0.0) -> int:
     """Cold problems: the centred fp32 path while few tile pairs need its fp64
-    fallback (``ctr_deferred``, a callable evaluated only then), else fp64;
+    fallback (``ctr_deferred``, a callable evaluated only then), else fp64
+    (with a measured block-sparse plan for large problems, CNTGW_F64S);
     otherwise the tensor cores where the shape allows."""
     forced = os.environ.get("CNTGW_PRECISION", "auto").lower()
     if forced in ("f32", "fp32"):
         return F32
     if forced in ("f64", "fp64"):
         return F64
+    if forced in ("f64s",):
+        return F64S
     if forced in ("tc", "tf32x3"):
         return TF32X3 if tc_supported(kd, sq) else F32
     if forced in ("f32c", "ctr"):
@@ -206,6 +256,8 @@ def choose_precision(scale: float, kd: int = 0, sq: bool = True, ctr_deferred=No
         if (ctr_deferred is not None and ctr_supported(kd, sq)
                 and os.environ.get("CNTGW_CTR", "1") != "0" and ctr_deferred() <= CTR_MAX_DEFERRED):
             return F32C
+        if pairs >= F64S_MIN_PAIRS and os.environ.get("CNTGW_F64S", "1") != "0":
+            return F64S
         return F64
     return TF32X3 if tc_supported(kd, sq) else F32
 
@@ -250,7 +302,7 @@ class Side:
 
     def locality(self) -> torch.Tensor:
         if self.order is None:
-            self.order = locality_order(_side_points(self))
+            self.order = side_order(self.feat64, self.sq64)
         return self.order
 
     @staticmethod
@@ -311,6 +363,7 @@ class HalfUpdate:
                                         dtype=torch.uint8, device=dev)
         wsb = max(LIB.cntgw_softmin_workspace(p, rows.n, cols.n, self.kd, int(self.sq)) for p in precs)
         self.ws = torch.empty(max(int(wsb), 16), dtype=torch.uint8, device=dev)
+        self.f64s_rows = None
 
     @property
     def prec(self) -> int:
@@ -318,9 +371,17 @@ class HalfUpdate:
 
     @prec.setter
     def prec(self, p: int):
-        if p == F32C:  # locality orders are computed eagerly, never inside a graph capture
+        if p in (F32C, F64S):  # orders and buffers are made eagerly, never inside a graph capture
             self.rows.locality()
             self.cols.locality()
+        if p == F64S:
+            r, c, dev = self.rows, self.cols, self.rows.feat64.device
+            if self.f64s_rows is None:
+                self.f64s_rows = torch.empty(int(LIB.cntgw_f64s_rows_bytes(r.n, self.kd)), dtype=torch.uint8,
+                                             device=dev)
+            need = int(LIB.cntgw_softmin_workspace(F64S, r.n, c.n, self.kd, int(self.sq)))
+            if self.ws.numel() < need:  # the measured plan (tmin per row and stage)
+                self.ws = torch.empty(need, dtype=torch.uint8, device=dev)
         self._prec = p
 
     def pack(self, state: SweepState, pot_cols: torch.Tensor | None, prec=None):
@@ -330,6 +391,11 @@ class HalfUpdate:
             call("cntgw_prep_cols_ctr", state.ptr, self.kd, int(self.sq), c.feat64.data_ptr(), self.kd,
                  _p(c.sq64 if self.sq else None), _p(pot_cols), c.log2w.data_ptr(),
                  c.locality().data_ptr(), c.n, self.ctr_cols.data_ptr(), _stream())
+            return
+        if prec == F64S:
+            call("cntgw_prep_cols_f64s", state.ptr, self.kd, int(self.sq), c.feat64.data_ptr(), self.kd,
+                 _p(c.sq64 if self.sq else None), _p(pot_cols), c.log2w.data_ptr(),
+                 c.locality().data_ptr(), c.n, self.rec.data_ptr(), _stream())
             return
         feat, sq = c.feat(prec)
         call("cntgw_prep_cols", state.ptr, prec, self.kd, int(self.sq), feat.data_ptr(), self.kd,
@@ -343,6 +409,11 @@ class HalfUpdate:
             call("cntgw_prep_rows_ctr", self.kd, int(self.sq), r.feat64.data_ptr(), self.kd, _p(sq),
                  r.locality().data_ptr(), r.n, self.ctr_rows.data_ptr(), _stream())
             feat, rec = self.ctr_rows, self.ctr_cols
+        elif self.prec == F64S:
+            sq = r.sq64 if self.sq else None
+            call("cntgw_prep_rows_f64s", self.kd, int(self.sq), r.feat64.data_ptr(), self.kd, _p(sq),
+                 r.locality().data_ptr(), r.n, self.f64s_rows.data_ptr(), _stream())
+            feat, rec = self.f64s_rows, self.rec
         else:
             feat, sq = r.feat(self.prec)
             rec = self.rec

@@ -259,7 +259,8 @@ def _set_precision(problem, eps, f0, g0):
                                   fwd.cols.sq64, pot)
     prec = engine.choose_precision(scale, fwd.kd, fwd.sq,
                                    ctr_deferred=lambda: engine.centred_choice_fraction(
-                                       eps, fwd.rows, fwd.cols))
+                                       eps, fwd.rows, fwd.cols),
+                                   pairs=float(fwd.rows.n) * float(fwd.cols.n))
     problem.fwd.prec = prec
     problem.bwd.prec = prec
 

@@ -34,7 +34,7 @@ import torch
 import torch.distributed as tdist
 
 from . import dist, divergence, engine
-from ._native import F32, F32C, F64, LIB, call
+from ._native import F32, F32C, F64, F64S, LIB, call
 from .measures import DenseCoupling, ImplicitCoupling
 from .sinkhorn import SinkhornConfig, SquaredEuclideanCost, sinkhorn
 
@@ -215,8 +215,8 @@ class _GwDevice:
             cols_feat = torch.zeros(self.m, self.kd, dtype=torch.float64, device=device)
         # locality orders of the point clouds (CNTGW_F32C tiles); the Gamma-dependent
         # features stay coherent along them (|Gamma dY| <= |Gamma| |dY|)
-        self.src = engine.Side(rows_feat, self.sx, self.a, order=engine.locality_order(self.x))
-        self.tgt = engine.Side(cols_feat, self.ty, self.b, order=engine.locality_order(self.y))
+        self.src = engine.Side(rows_feat, self.sx, self.a, order=engine.side_order(self.x, None))
+        self.tgt = engine.Side(cols_feat, self.ty, self.b, order=engine.side_order(self.y, None))
         self.fwd = engine.HalfUpdate(self.src, self.tgt, True)
         self.bwd = engine.HalfUpdate(self.tgt, self.src, True)
         self.loop = engine.SinkhornLoop(self.fwd, self.bwd, self.a, self.b, device, comm=self.comm)
@@ -266,7 +266,8 @@ class _GwDevice:
         On the centred path (CNTGW_F32C) the pass reuses the f-half-update's
         block-sparse plan (cntgw_plan_reduce_ctr: rows and columns in locality
         order, tiles that cannot hold a term within 2^-64 of a row's maximum
-        skipped); otherwise it is the dense fp64 pass (cntgw_plan_reduce).
+        skipped), on CNTGW_F64S its measured plan (cntgw_plan_reduce_f64s)
+        while it holds; otherwise it is the dense fp64 pass (cntgw_plan_reduce).
         CNTGW_K4_SPARSE=0 forces the dense pass."""
         st = self.loop.state
         stream = _stream()
@@ -280,6 +281,18 @@ class _GwDevice:
                  fwd.ctr_cols.data_ptr(), self.tgt.locality().data_ptr(), src.feat64.data_ptr(),
                  fwd.kd, self.sx.data_ptr(), f.data_ptr(), src.log2w.data_ptr(), self.y.data_ptr(),
                  self.e, self.ty.data_ptr(), self.n, self.m, self.r.data_ptr(), self.pi_y.data_ptr(),
+                 self.pi_s.data_ptr(), self.argmax.data_ptr(), fwd.ws.data_ptr(), fwd.ws.numel(),
+                 self.ws_plan.data_ptr(), self.ws_plan.numel(), stream)
+            return
+        if self.prec == F64S and os.environ.get("CNTGW_K4_SPARSE", "1") != "0":
+            src = self.src
+            call("cntgw_prep_rows_f64s", fwd.kd, 1, src.feat64.data_ptr(), fwd.kd, src.sq64.data_ptr(),
+                 src.locality().data_ptr(), src.n, fwd.f64s_rows.data_ptr(), stream)
+            fwd.pack(st, g, prec=F64S)
+            call("cntgw_plan_reduce_f64s", st.ptr, fwd.kd, 1, self.e, fwd.f64s_rows.data_ptr(),
+                 fwd.rec.data_ptr(), self.tgt.locality().data_ptr(), src.feat64.data_ptr(), fwd.kd,
+                 self.sx.data_ptr(), f.data_ptr(), src.log2w.data_ptr(), self.y.data_ptr(), self.e,
+                 self.ty.data_ptr(), self.n, self.m, self.r.data_ptr(), self.pi_y.data_ptr(),
                  self.pi_s.data_ptr(), self.argmax.data_ptr(), fwd.ws.data_ptr(), fwd.ws.numel(),
                  self.ws_plan.data_ptr(), self.ws_plan.numel(), stream)
             return
@@ -341,7 +354,8 @@ class _GwDevice:
         else:
             scale = engine.exponent_scale(eps_min, self.src.feat64, self.sx, self.tgt.feat64, self.ty, pot)
         self.prec = engine.choose_precision(
-            scale, self.kd, True, ctr_deferred=lambda: self._ctr_deferred(eps_min))
+            scale, self.kd, True, ctr_deferred=lambda: self._ctr_deferred(eps_min),
+            pairs=float(self.n_total) * float(self.m))
         self.loop.set_precision(self.prec)
 
     def reachable_scale(self, eps: float, pot_abs: float) -> float:

@@ -52,7 +52,7 @@ def _half_update(env, cost, a, b, g, eps, prec=None):
 
 # "f32c" runs the centred path's FFMA2 kernel (the default); "f32c_tc" its
 # opt-in tcgen05 kernel where kd + sq <= 4 (CNTGW_CTR_TC=1)
-PRECS = {"f32": 0, "f64": 1, "f32c": 3, "f32c_tc": 3}
+PRECS = {"f32": 0, "f64": 1, "f32c": 3, "f32c_tc": 3, "f64s": 4}
 
 
 def _prec(name, monkeypatch):
@@ -79,7 +79,7 @@ def test_sq_euclidean_half_update(env, k, n, m, pname, monkeypatch):
     eps = 0.05
     got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, prec)
     want = O.softmin(O.SqEuclid(x, z), np.log(b), g, eps)
-    assert _rel(got, want) < (5e-7 if prec == 1 else 1e-5)
+    assert _rel(got, want) < (5e-7 if prec in (1, 4) else 1e-5)
 
 
 @pytest.mark.parametrize("k", [4, 16])
@@ -108,7 +108,7 @@ def test_rebase_path_under_huge_exponents(env, pname, monkeypatch):
     eps = 1.25e-3
     got = _half_update(env, P.SquaredEuclideanCost(x, z), a, b, g, eps, prec)
     want = O.softmin(O.SqEuclid(x, z), np.log(b), g, eps)
-    assert _rel(got, want) < (5e-7 if prec == 1 else 1e-5)
+    assert _rel(got, want) < (5e-7 if prec in (1, 4) else 1e-5)
 
 
 @pytest.mark.parametrize("tc", ["1", "0"], ids=["tcgen05", "ffma"])
@@ -334,3 +334,36 @@ def test_centred_plan_reuse_across_sweeps(env, anneal, monkeypatch):
     for tag in ("replan", "dense"):
         assert _rel(out["reuse"][0], out[tag][0]) < 1e-9, tag
         assert _rel(out["reuse"][1], out[tag][1]) < 1e-9, tag
+
+
+@pytest.mark.parametrize("anneal", [None, 0.05], ids=["fixed", "annealed"])
+@pytest.mark.parametrize("k", [3, 32])
+def test_f64s_measured_plan_matches_dense_loop(env, k, anneal, monkeypatch):
+    """CNTGW_F64S: fp64 DMMA sweeps on cluster-ordered rows/columns that skip
+    the (row group, stage) pairs a measured plan found below 2^-80 of every
+    row's maximum. A whole Sinkhorn loop (plan reused across sweeps, replanned
+    when a column record drifts or lam changes under annealing) equals the
+    dense fp64 loop; outputs come back in the caller's order."""
+    P, engine, S, O, torch, dev = env
+    rng = np.random.default_rng(31 + k)
+    n, m = 1 << 14, 3 << 12
+    cx = rng.standard_normal((16, k)) * 2.0
+    x = cx[rng.integers(0, 16, n)] + rng.standard_normal((n, k)) * 0.5
+    z = cx[rng.integers(0, 16, m)] @ np.linalg.qr(rng.standard_normal((k, k)))[0] \
+        + rng.standard_normal((m, k)) * 0.5
+    a, b = np.full(n, 1 / n), np.full(m, 1 / m)
+    cost = P.SquaredEuclideanCost(x, z)
+    cfg = P.SinkhornConfig(eps=2.5e-3, n_inner=30, anneal_from=anneal)
+    out = {}
+    for prec in ("f64s", "f64"):
+        monkeypatch.setenv("CNTGW_PRECISION", prec)
+        res = P.sinkhorn(a, b, cost, cfg)
+        out[prec] = (res.coupling.f, res.coupling.g)
+    # (the two paths visit columns in different orders, and both sum
+    # 2^(fp64 offset truncated to fp32) per term: ~1e-9 relative apart)
+    assert _rel(out["f64s"][0], out["f64"][0]) < 1e-8
+    assert _rel(out["f64s"][1], out["f64"][1]) < 1e-8
+    rows = np.sort(rng.choice(n, 64, replace=False))
+    want = O.softmin(O.SqEuclid(x, z), np.log(b), out["f64s"][1], res.coupling.eps_eff, row_idx=rows)
+    got = _half_update(env, cost, a, b, out["f64s"][1], res.coupling.eps_eff, 4)
+    assert _rel(got[rows], want) < 5e-7

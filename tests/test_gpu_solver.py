@@ -315,7 +315,8 @@ def test_c4_full_size_centred_half_updates_match_fp64(P, monkeypatch):
         assert np.percentile(np.abs(a - b) * lam, 99) < 1e-3
 
 
-def test_block_sparse_k4_matches_dense(P, monkeypatch):
+@pytest.mark.parametrize("path", ["f32c", "f64s"])
+def test_block_sparse_k4_matches_dense(P, path, monkeypatch):
     """K4 on the centred path's block-sparse plan (cntgw_plan_reduce_ctr)
     against the dense fp64 K4 (cntgw_plan_reduce) on the SAME final pair:
     C4 law, N=M=2^16, after an outer step on the centred path. Skipped tiles
@@ -326,11 +327,14 @@ def test_block_sparse_k4_matches_dense(P, monkeypatch):
     outer steps with either pass agree to the centred kernel's fp32 noise."""
     from paper_2602_06658_b200 import configs, solvers
 
-    pc = configs.c4(seed=2, n=1 << 16)
-    src = P.embed_measure(P.DiscreteMeasure(pc.x, pc.a), P.CostSpec("sq_euclidean"), dim=3)
-    tgt = P.embed_measure(P.DiscreteMeasure(pc.y, pc.b), P.CostSpec("sq_euclidean"), dim=3)
-    monkeypatch.setenv("CNTGW_PRECISION", "f32c")
-    st = solvers._CntGwState(src, tgt, P.make_config(configs.C4_EPS, n_inner=30, max_outer=2))
+    if path == "f32c":  # C4 law, the centred path's geometric plan
+        pc, eps, dims = configs.c4(seed=2, n=1 << 16), configs.C4_EPS, (3, 3)
+    else:  # C5 law, CNTGW_F64S's measured plan
+        pc, eps, dims = configs.c5(seed=2, n=1 << 14), configs.C5_EPS, (64, 32)
+    src = P.embed_measure(P.DiscreteMeasure(pc.x, pc.a), P.CostSpec("sq_euclidean"), dim=dims[0])
+    tgt = P.embed_measure(P.DiscreteMeasure(pc.y, pc.b), P.CostSpec("sq_euclidean"), dim=dims[1])
+    monkeypatch.setenv("CNTGW_PRECISION", path)
+    st = solvers._CntGwState(src, tgt, P.make_config(eps, n_inner=30, max_outer=2))
     st.step()
     st.step()
     dev = st.dev
@@ -350,7 +354,7 @@ def test_block_sparse_k4_matches_dense(P, monkeypatch):
     traj = {}
     for flag in ("1", "0"):
         monkeypatch.setenv("CNTGW_K4_SPARSE", flag)
-        s2 = solvers._CntGwState(src, tgt, P.make_config(configs.C4_EPS, n_inner=30, max_outer=2))
+        s2 = solvers._CntGwState(src, tgt, P.make_config(eps, n_inner=30, max_outer=2))
         objs = [s2.step().objective for _ in range(2)]
         traj[flag] = (np.array(objs), s2.gamma.copy())
     assert _rel(traj["1"][0], traj["0"][0]) < 1e-6
