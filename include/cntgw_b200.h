@@ -199,6 +199,10 @@ int cntgw_prep_cols_ctr(const cntgw_sweep_state* st, int kd, int sq_flag, const 
 size_t cntgw_f64s_rows_bytes(int64_t n, int kd);
 int cntgw_prep_rows_f64s(int kd, int sq_flag, const double* feat, int64_t ld, const double* sq,
                          const int64_t* order, int64_t n, void* rows, void* stream);
+/* Diagnostics of the plan in an F64S workspace: out (3 int64, device) =
+ * [needed (row group, stage) pairs, all pairs, 1 if the last sweep measured]. */
+int cntgw_f64s_plan_density(int kd, int sq_flag, int64_t n, int64_t m, const void* workspace, int64_t* out,
+                            void* stream);
 /* cntgw_prep_cols (CNTGW_F64 records) with the columns gathered in `order`. */
 int cntgw_prep_cols_f64s(const cntgw_sweep_state* st, int kd, int sq_flag, const double* feat, int64_t ld,
                          const double* sq, const double* pot, const double* log2w, const int64_t* order,

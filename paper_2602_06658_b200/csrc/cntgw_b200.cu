@@ -223,7 +223,7 @@ size_t ctr_plan_bytes(const KernelPick& k, int64_t n, int64_t m) {
 // Measured plan of the CNTGW_F64S kernel: tmin [n][stages] fp32, need
 // [row tiles][stages] bytes, c at the last plan [mpad] fp64, CtrPlanKey.
 struct F64sPlanLayout {
-  size_t tmin, need, cplan, total;
+  size_t tmin, need, cplan, range, total;
   int stages;
   int64_t row_tiles;
 };
@@ -236,8 +236,56 @@ F64sPlanLayout f64s_layout(const KernelPick& k, int64_t n, int64_t m) {
   l.tmin = align256(sizeof(float) * (size_t)n * l.stages);
   l.need = align256((size_t)l.row_tiles * l.stages);
   l.cplan = align256(sizeof(double) * (size_t)mpad);
-  l.total = l.tmin + l.need + l.cplan + 256;
+  l.range = align256(sizeof(double2) * (size_t)l.stages);
+  l.total = l.tmin + l.need + l.cplan + l.range + 256;  // + CtrPlanKey, flag, counter
   return l;
+}
+
+// Pointers into the F64S plan workspace (after the split-column partials).
+struct F64sPlan {
+  float* tmin;
+  uint8_t* need;
+  double* c_plan;
+  double2* range;
+  CtrPlanKey* key;
+  int* flag;
+  int* counter;
+  int* next_measure;
+};
+F64sPlan f64s_plan(void* base_v, const F64sPlanLayout& l) {
+  char* base = static_cast<char*>(base_v);
+  F64sPlan p;
+  p.tmin = reinterpret_cast<float*>(base);
+  p.need = reinterpret_cast<uint8_t*>(base + l.tmin);
+  p.c_plan = reinterpret_cast<double*>(base + l.tmin + l.need);
+  p.range = reinterpret_cast<double2*>(base + l.tmin + l.need + l.cplan);
+  p.key = reinterpret_cast<CtrPlanKey*>(base + l.tmin + l.need + l.cplan + l.range);
+  p.flag = &p.key->replan;
+  p.counter = reinterpret_cast<int*>(reinterpret_cast<char*>(p.key) + 128);
+  p.next_measure = p.counter + 1;
+  return p;
+}
+
+// Re-vote the measured plan for the current records (f64s_* kernels,
+// softmin_f64s.cuh); leaves *flag = 1 when the sweep must measure anew (or,
+// for a consumer such as K4, walk every stage).
+int f64s_revote(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl, const cntgw_sweep_state* st,
+                const double* rec, int kd, int sq, const void* rows, const void* cols, int64_t n, int64_t m,
+                cudaStream_t s, int schedule) {
+  const int stride = (kd + sq + 1 + 1) / 2 * 2 > (kd + sq + 3) / 4 * 4 ? (kd + sq + 1 + 1) / 2 * 2
+                                                                       : (kd + sq + 3) / 4 * 4;
+  f64s_begin_kernel<<<1, 1, 0, s>>>(st, pl.key, rows, cols, n, m, pl.flag, pl.counter);
+  f64s_shift_kernel<<<(unsigned)l.stages, 128, 0, s>>>(rec, stride, kd + sq, m, k.f64s_tile, pl.c_plan, pl.range,
+                                                        pl.flag);
+  const char* te = getenv("CNTGW_CTR_SKIP_T");
+  const double T = te ? atof(te) : 64.0;
+  f64s_vote_kernel<<<(unsigned)l.row_tiles, 256, sizeof(double) * k.cta_rows, s>>>(
+      pl.flag, pl.tmin, pl.range, n, l.stages, k.cta_rows, T, pl.need, pl.counter);
+  const char* fe = getenv("CNTGW_F64S_REMEASURE");
+  const double frac = fe ? atof(fe) : 0.25;
+  f64s_decide_kernel<<<1, 1, 0, s>>>(st, pl.flag, pl.counter, pl.next_measure, l.row_tiles * (int64_t)l.stages,
+                                     frac, schedule);
+  return check_launch("f64s_revote");
 }
 size_t f64s_plan_bytes(const KernelPick& k, int64_t n, int64_t m) { return f64s_layout(k, n, m).total; }
 
@@ -747,37 +795,33 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
     a.ctr_need = ctr_build_plan(k, a, static_cast<char*>(workspace) + part_bytes, s);
   F64sArgs fs{};
   F64sPlanLayout fl{};
-  if (k.f64s_tile > 0) {  // CNTGW_F64S: plan check, then the sweep (dense + measure, or sparse)
+  if (k.f64s_tile > 0) {  // CNTGW_F64S: re-vote the plan, then the sweep (measure, or sparse)
     fl = f64s_layout(k, n, m);
     if (p.chunk_cols / k.f64s_tile > 4096)
       return fail(CNTGW_EINVAL, "softmin f64s: %lld stages per column chunk (max 4096)",
                   (long long)(p.chunk_cols / k.f64s_tile));
-    char* base = static_cast<char*>(workspace) + part_bytes;
-    fs.tmin = reinterpret_cast<float*>(base);
-    uint8_t* need_w = reinterpret_cast<uint8_t*>(base + fl.tmin);
-    fs.need = need_w;
-    double* c_plan = reinterpret_cast<double*>(base + fl.tmin + fl.need);
-    CtrPlanKey* key = reinterpret_cast<CtrPlanKey*>(base + fl.tmin + fl.need + fl.cplan);
+    const F64sPlan pl = f64s_plan(static_cast<char*>(workspace) + part_bytes, fl);
+    fs.tmin = pl.tmin;
+    fs.need = pl.need;
     fs.row_order = static_cast<const int64_t*>(row_feat);  // the rows block starts with the order
-    fs.replan = &key->replan;
+    fs.replan = pl.flag;
     fs.stages = fl.stages;
-    const int64_t mpad = (m + kColTile - 1) / kColTile * kColTile;
-    const int stride = cntgw_col_stride(CNTGW_F64S, kd, sq_flag);
-    // CNTGW_CTR_REUSE=0: a fresh measured plan every call (budget < 0)
-    const double budget = env_int("CNTGW_CTR_REUSE", 1) != 0 ? 8.0 : -1.0;
-    f64s_check_kernel<<<1, 1024, 0, s>>>(st, static_cast<const double*>(col_rec), stride, kd + (sq_flag ? 1 : 0),
-                                         mpad, c_plan, key, row_feat, col_rec, n, m, budget, &key->replan, 1);
+    const double* rec = static_cast<const double*>(col_rec);
+    if (const int rc = f64s_revote(k, fl, pl, st, rec, kd, sq_flag ? 1 : 0, row_feat, col_rec, n, m, s, 1))
+      return rc;
+    if (env_int("CNTGW_CTR_REUSE", 1) == 0) f64s_begin_kernel<<<1, 1, 0, s>>>(nullptr, pl.key, row_feat, col_rec,
+                                                                                n, m, pl.flag, pl.counter);
     void* args2[] = {&a, &fs};
     cudaError_t e2 = cudaLaunchKernel(k.fn, dim3(p.row_tiles, p.nchunks), dim3(k.threads), args2, k.smem, s);
     if (e2 != cudaSuccess) {
       cudaGetLastError();
       return fail(CNTGW_ECUDA, "softmin f64s launch: %s", cudaGetErrorString(e2));
     }
-    const char* te = getenv("CNTGW_CTR_SKIP_T");
-    const float Tp = (float)((te ? atof(te) : 64.0) + 2.0 * (budget > 0 ? budget : 0.0));
-    f64s_vote_kernel<<<(unsigned)fl.row_tiles, 256, sizeof(float) * k.cta_rows, s>>>(
-        fs.replan, fs.tmin, n, fl.stages, k.cta_rows, Tp, need_w);
-    if (const int rc = check_launch("f64s_vote")) return rc;
+    const int64_t mpad = (m + kColTile - 1) / kColTile * kColTile;
+    f64s_commit_kernel<<<1, 1024, 0, s>>>(pl.flag, st, rec, cntgw_col_stride(CNTGW_F64S, kd, sq_flag),
+                                          kd + (sq_flag ? 1 : 0), mpad, pl.c_plan, pl.key, row_feat, col_rec, n, m,
+                                          pl.next_measure);
+    if (const int rc = check_launch("f64s_commit")) return rc;
     if (p.nchunks > 1) {
       const int th = 256;
       lse_combine_kernel<<<(unsigned)((n + th - 1) / th), th, 0, s>>>(
@@ -821,6 +865,23 @@ int cntgw_softmin_dense(const cntgw_sweep_state* st, int skip_if_done, const dou
   softmin_dense_kernel<<<(unsigned)((n + warps - 1) / warps), warps * 32, 0, as_stream(stream)>>>(
       st, skip_if_done, cost, ld, pot, log2w, row_add, n, m, out);
   return check_launch("softmin_dense");
+}
+
+/* ---- CNTGW_F64S plan diagnostics: out[0] needed (row group, stage) pairs of
+ * the mask the last sweep used, out[1] all pairs, out[2] 1 if that sweep
+ * measured (walked every stage); out: 3 int64 on the device (out[0] summed) */
+int cntgw_f64s_plan_density(int kd, int sq_flag, int64_t n, int64_t m, const void* workspace, int64_t* out,
+                            void* stream) {
+  KernelPick k;
+  if (!workspace || !out || n < 1 || m < 1 || !lookup(CNTGW_F64S, kd, sq_flag, &k))
+    return fail(CNTGW_EINVAL, "f64s_plan_density: bad arguments");
+  const F64sPlanLayout fl = f64s_layout(k, n, m);
+  const size_t part_bytes = align256(plan_workspace(plan_softmin(n, m, k), n));
+  const F64sPlan pl = f64s_plan(static_cast<char*>(const_cast<void*>(workspace)) + part_bytes, fl);
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(out, 0, sizeof(int64_t), s);
+  f64s_density_kernel<<<148, 256, 0, s>>>(pl.need, fl.row_tiles * (int64_t)fl.stages, pl.flag, out);
+  return check_launch("f64s_density");
 }
 
 /* ---- CNTGW_F64S rows block and ordered column records ---- */
@@ -923,7 +984,7 @@ int cntgw_plan_reduce_ctr(const cntgw_sweep_state* st, int kd, int sq_flag, int 
 #define PRC(KX_, E_)                                                                    \
   if (kx == KX_ && ep == E_) {                                                         \
     auto kern = plan_reduce_ctr_kernel<KX_, E_, 4>;                                    \
-    const size_t smem = CtrReduceSmem<KX_, E_>::kBytes;                                \
+    const size_t smem = CtrReduceSmem<KX_ + 1, E_>::kBytes;                                \
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     kern<<<blocks, 128, smem, s>>>(a);                                                 \
     return check_launch("plan_reduce_ctr_kernel");                                     \
@@ -956,17 +1017,12 @@ int cntgw_plan_reduce_f64s(const cntgw_sweep_state* st, int kd, int sq_flag, int
   if (plan_ws_bytes < part_bytes + fl.total)
     return fail(CNTGW_ENOSPACE, "plan_reduce_f64s: plan workspace %zu < %zu", plan_ws_bytes, part_bytes + fl.total);
   cudaStream_t s = as_stream(stream);
-  char* base = static_cast<char*>(plan_ws) + part_bytes;
-  const uint8_t* need = reinterpret_cast<const uint8_t*>(base + fl.tmin);
-  double* c_plan = reinterpret_cast<double*>(base + fl.tmin + fl.need);
-  CtrPlanKey* key = reinterpret_cast<CtrPlanKey*>(base + fl.tmin + fl.need + fl.cplan);
-  int* stale = &key->pad_;  // this pass's own verdict (the half-update's flag is left alone)
+  const F64sPlan pl = f64s_plan(static_cast<char*>(plan_ws) + part_bytes, fl);
   const int64_t mpad = cntgw_cols_padded(m);
-  const int stride = cntgw_col_stride(CNTGW_F64S, kd, 1);
-  const double budget = env_int("CNTGW_CTR_REUSE", 1) != 0 ? 8.0 : -1.0;
-  f64s_check_kernel<<<1, 1024, 0, s>>>(st, col_rec, stride, kd + 1, mpad, c_plan, key, f64s_rows, col_rec, n, m,
-                                       budget, stale, 0);
-  if (const int rc = check_launch("f64s_check")) return rc;
+  // re-vote for the final pair's records; a stale plan (*flag) walks every stage
+  if (const int rc = f64s_revote(k, fl, pl, st, col_rec, kd, 1, f64s_rows, col_rec, n, m, s, 0)) return rc;
+  const uint8_t* need = pl.need;
+  const int* stale = pl.flag;
   const int stride_acc = (ep + 1 + 1) / 2 * 2;
   double* acc = static_cast<double*>(acc_ws);
   pack_acc_ordered_kernel<<<(unsigned)((mpad + 255) / 256), 256, 0, s>>>(col_acc, ld_acc, e, ep, stride_acc, col_s,

@@ -10,22 +10,19 @@
 // gathered into a block in the caller-supplied order (cntgw_prep_rows_f64s)
 // and the results scattered back; column records are packed in the column
 // order (cntgw_prep_cols_f64s). A plan is a per-(CTA row group, column
-// stage) mask measured, not bounded:
-//   * replan sweep (the first sweep of a loop, a new operator or lam, or
-//     column records whose shifts since the plan spread over more than
-//     2 budget log2 units, f64s_check_kernel): the kernel walks every stage — the sweep's
-//     outputs are exact — and also writes each row's minimum q over each
-//     stage (tmin, fp32 rounded down); f64s_vote_kernel then marks a stage
-//     needed by a row group when one of its rows has a term within
-//     T + 2 budget log2 units of the row's maximum (T = 64);
-//   * other sweeps walk only the needed stages (their compacted list is
-//     built in shared memory, so the bulk-copy ring stays dense).
-// A term skipped under a plan made with threshold T + 2 budget stays below
-// 2^-T of its row's maximum while max_j d_j - min_j d_j <= 2 budget, d_j the
-// change of column j's record constant -beta_j since the plan (every term of
-// column j shifts by exactly d_j, the row's maximum by the d of some other
-// column), so the skipped mass is < m 2^-64 of every row's sum. On the C5
-// law 4-8% of the (row group, stage) pairs are needed (tools/c5_sparsity.py).
+// stage) mask derived from MEASURED stage minima, not from geometric bounds:
+//   * a measuring sweep (the first of a loop, see below) walks every stage —
+//     its outputs are exact — and also writes each row's minimum q over each
+//     stage (tmin, fp32 rounded down);
+//   * every later sweep re-votes the mask from tmin and the per-stage range
+//     of the column-constant shifts since the measurement (f64s_shift /
+//     f64s_vote kernels, below) and walks only the needed stages (their
+//     compacted list is built in shared memory, so the bulk-copy ring stays
+//     dense).
+// Skipped terms are below 2^-64 of their row's maximum (exact bounds, no
+// assumption on how the potentials move), so the skipped mass is < m 2^-64
+// of every row's sum. On the C5 law 8% of the (row group, stage) pairs are
+// needed right after a measurement (tools/c5_sparsity.py).
 #pragma once
 
 #include "common.cuh"
@@ -62,94 +59,147 @@ __global__ void f64s_prep_rows_kernel(int kd, int sq_flag, const double* feat, i
   s[i] = sq_flag ? sq[src] : 0.0;
 }
 
-// Plan reuse check for the fp64 records: the column constant -beta_j sits at
-// `off` in records of `stride` doubles (same rules as ctr_plan_check_kernel).
-__global__ void __launch_bounds__(1024) f64s_check_kernel(const cntgw_sweep_state* st, const double* rec,
-                                                          int stride, int off, int64_t mpad, double* c_plan,
-                                                          CtrPlanKey* key, const void* rows, const void* cols,
-                                                          int64_t n, int64_t m, double budget,
-                                                          int* flag_out, int commit) {
-  __shared__ double red[32], red2[32];
-  __shared__ int go, nan_seen;
+// ---- the measured plan, re-voted every sweep ---------------------------------
+// State (workspace, f64s_layout): tmin[n][stages] — each row's minimum q over
+// each stage at the last MEASURED sweep — and c_plan, the column constants
+// -beta_j at that sweep. Every later sweep sees column shifts d_j = c_j -
+// c_plan_j; with [dmin_t, dmax_t] their range over stage t, the current
+//   stage minimum >= tmin[i][t] + dmin_t,
+//   row minimum   <= U_i = min_t (tmin[i][t] + dmax_t),
+// so a stage with tmin[i][t] + dmin_t > U_i + T for every row of a group
+// holds only terms below 2^-T of each row's maximum and is skipped. Uniform
+// drifts cancel exactly, and per-stage ranges stay narrow while the global
+// spread of the shifts is large (a stage is 64-256 columns of one cluster).
+// A sweep measures anew (dense, tmin rewritten) on the first sweep of a
+// loop, for a new operator or lam, on a NaN record, or when the re-vote
+// keeps more than CNTGW_F64S_REMEASURE of the (group, stage) pairs.
+
+// (1 block) replan = first sweep / new key; the counter of needed pairs = 0
+__global__ void f64s_begin_kernel(const cntgw_sweep_state* st, CtrPlanKey* key, const void* rows,
+                                  const void* cols, int64_t n, int64_t m, int* flag, int* counter) {
   const double lam = st ? st->lam_d : 0.0;
   const bool first = st == nullptr || st->sweep <= 1 || key->lam != lam || key->rows != rows ||
                      key->cols != cols || key->n != n || key->m != m;
-  if (threadIdx.x == 0) nan_seen = 0;
-  __syncthreads();
-  // validity of the plan: a term skipped with margin T + 2 budget moved by
-  // its column's shift d_j = c_j - c_j(plan), its row's maximum by the shift
-  // of another column, so the plan holds while max_j d_j - min_j d_j <=
-  // 2 budget (a uniform shift of every column changes nothing)
-  double dmx = 0.0, dmn = 0.0;
+  *flag = first ? 1 : 0;
+  *counter = 0;
+}
+
+// one block per stage: the range of the column shifts over the stage's real
+// columns (+inf / -inf when it has none: never needed, never bounds a row);
+// a NaN record or planned constant forces a measurement
+__global__ void __launch_bounds__(128) f64s_shift_kernel(const double* rec, int stride, int off, int64_t m,
+                                                         int tile, const double* c_plan, double2* range,
+                                                         int* flag) {
+  __shared__ double smn[4], smx[4];
+  const int64_t j0 = (int64_t)blockIdx.x * tile;
+  double mn = CUDART_INF, mx = -CUDART_INF;
   bool bad = false;
-  if (!first)
-    for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
-      const double c = rec[j * stride + off], cp = c_plan[j];
-      bad |= (c != c) || (cp != cp);
-      const double d = c == cp ? 0.0 : c - cp;  // equal infinities (zero weight): no change
-      dmx = fmax(dmx, d);
-      dmn = fmin(dmn, d);
-    }
-  if (bad) nan_seen = 1;  // fmax/fmin drop NaN, so it is flagged separately
+  for (int u = threadIdx.x; u < tile; u += blockDim.x) {
+    const int64_t j = j0 + u;
+    if (j >= m) break;
+    const double c = rec[j * stride + off], cp = c_plan[j];
+    bad |= (c != c) || (cp != cp);
+    if (c == cp && !(c < CUDART_INF && c > -CUDART_INF)) continue;  // zero weight: no term at all
+    const double d = c == cp ? 0.0 : c - cp;
+    mn = fmin(mn, d);
+    mx = fmax(mx, d);
+  }
+  if (bad) atomicOr(flag, 1);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
-    dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   }
   if ((threadIdx.x & 31) == 0) {
-    red[threadIdx.x >> 5] = dmx;
-    red2[threadIdx.x >> 5] = dmn;
+    smn[threadIdx.x >> 5] = mn;
+    smx[threadIdx.x >> 5] = mx;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double mx = 0.0, mn = 0.0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
-      mx = fmax(mx, red[q]);
-      mn = fmin(mn, red2[q]);
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      mn = fmin(mn, smn[w]);
+      mx = fmax(mx, smx[w]);
     }
-    go = (first || nan_seen || !(mx - mn <= 2.0 * budget)) ? 1 : 0;
-    *flag_out = go;
-    if (go && commit) {
-      key->lam = lam;
-      key->rows = rows;
-      key->cols = cols;
-      key->n = n;
-      key->m = m;
-    }
+    range[blockIdx.x] = make_double2(mn, mx);
   }
-  __syncthreads();
-  // commit = 0: a consumer of the plan (K4) only asks whether it still holds
-  if (go && commit)
-    for (int64_t j = threadIdx.x; j < mpad; j += blockDim.x) c_plan[j] = rec[j * stride + off];
 }
 
-// One block per row group of `grows` rows: each row's minimum over the stage
-// minima (its maximum term), then per stage an OR over the group's rows of
-// "holds a term within Tp of the row maximum" (NaN counts as needed).
-__global__ void __launch_bounds__(256) f64s_vote_kernel(const int* replan, const float* tmin, int64_t n,
-                                                        int stages, int grows, float Tp, uint8_t* need) {
-  if (!*replan) return;
-  extern __shared__ float rowmin[];  // [grows]
+// One block per row group of `grows` rows (skipped on a measuring sweep): the
+// rows' upper bounds U_i, then per stage an OR over the group's rows of
+// "tmin + dmin <= U + T" (NaN keeps the stage); counts the needed pairs.
+__global__ void __launch_bounds__(256) f64s_vote_kernel(const int* flag, const float* tmin,
+                                                        const double2* range, int64_t n, int stages, int grows,
+                                                        double T, uint8_t* need, int* counter) {
+  if (*flag) return;
+  extern __shared__ double ub[];  // [grows]
   const int64_t r0 = (int64_t)blockIdx.x * grows;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int r = warp; r < grows; r += nw) {
-    float mn = CUDART_INF_F;
+    double u = CUDART_INF;
     if (r0 + r < n)
-      for (int t = lane; t < stages; t += 32) mn = fminf(mn, tmin[(r0 + r) * stages + t]);
+      for (int t = lane; t < stages; t += 32) u = fmin(u, (double)tmin[(r0 + r) * stages + t] + range[t].y);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    if (lane == 0) rowmin[r] = mn;
+    for (int o = 16; o > 0; o >>= 1) u = fmin(u, __shfl_xor_sync(0xffffffffu, u, o));
+    // tmin is rounded down (at most 2^-23 relative): widen the upper bound
+    if (lane == 0) ub[r] = u + fabs(u) * 0x1p-21;
   }
   __syncthreads();
+  int cnt = 0;
   for (int t = threadIdx.x; t < stages; t += blockDim.x) {
     uint8_t v = 0;
-    for (int r = 0; r < grows && r0 + r < n && !v; ++r) {
-      const float q = tmin[(r0 + r) * stages + t], mn = rowmin[r];
-      // tmin and rowmin are rounded down; the allowance covers the fp32
-      // rounding of the sum (NaN keeps the stage)
-      v = !(q > mn + Tp + fabsf(mn) * 0x1p-20f) ? 1 : 0;
-    }
+    const double dmin = range[t].x;
+    for (int r = 0; r < grows && r0 + r < n && !v; ++r)
+      v = !((double)tmin[(r0 + r) * stages + t] + dmin > ub[r] + T) ? 1 : 0;
     need[(int64_t)blockIdx.x * stages + t] = v;
+    cnt += v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0 && cnt) atomicAdd(counter, cnt);
+}
+
+// (1 thread) measure anew when the re-vote kept too much, and on a geometric
+// schedule (sweeps 8, 16, 32, ... of a loop) while it keeps more than 2%: the
+// plan measured early in a loop reflects transient potentials, and the
+// re-vote only ever loosens it (a measurement costs ~1.2 dense sweeps)
+__global__ void f64s_decide_kernel(const cntgw_sweep_state* st, int* flag, const int* counter,
+                                   const int* next_measure, int64_t pairs, double max_frac, int schedule) {
+  if (*flag) return;
+  const double kept = (double)*counter / (double)pairs;
+  const int sweep = st ? st->sweep : 0;
+  if (kept > max_frac || (schedule && sweep >= *next_measure && kept > 0.02)) *flag = 1;
+}
+
+// diagnostics: needed (group, stage) pairs of the current mask and the flag
+__global__ void f64s_density_kernel(const uint8_t* need, int64_t pairs, const int* flag, int64_t* out) {
+  int64_t c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += (int64_t)gridDim.x * blockDim.x)
+    c += need[i] ? 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)c);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out[1] = pairs;
+    out[2] = *flag;
+  }
+}
+
+// after a measuring sweep: the plan's reference constants and key
+__global__ void __launch_bounds__(1024) f64s_commit_kernel(const int* flag, const cntgw_sweep_state* st,
+                                                           const double* rec, int stride, int off, int64_t mpad,
+                                                           double* c_plan, CtrPlanKey* key, const void* rows,
+                                                           const void* cols, int64_t n, int64_t m,
+                                                           int* next_measure) {
+  if (!*flag) return;
+  for (int64_t j = threadIdx.x; j < mpad; j += blockDim.x) c_plan[j] = rec[j * stride + off];
+  if (threadIdx.x == 0) {
+    const int sweep = st ? st->sweep : 0;
+    *next_measure = 2 * sweep > 8 ? 2 * sweep : 8;
+    key->lam = st ? st->lam_d : 0.0;
+    key->rows = rows;
+    key->cols = cols;
+    key->n = n;
+    key->m = m;
   }
 }
 

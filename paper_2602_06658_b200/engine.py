@@ -133,12 +133,15 @@ def locality_order(coords: torch.Tensor) -> torch.Tensor:
     return torch.sort(codes, stable=True).indices
 
 
-def cluster_order(points: torch.Tensor, k: int = 64, sweeps: int = 8, seed: int = 0) -> torch.Tensor:
+def cluster_order(points: torch.Tensor, sq: torch.Tensor | None = None, k: int = 64, sweeps: int = 8,
+                  seed: int = 0) -> torch.Tensor:
     """Permutation grouping high-dimensional points by a k-means clustering
     (CNTGW_F64S row groups / column stages): k seeded centres, `sweeps`
     Lloyd iterations (streamed assignment ``cntgw_km_assign``; centres as a
-    one-hot fp64 GEMM, deterministic), then points sorted by (cluster, Morton
-    code of their first coordinates)."""
+    one-hot fp64 GEMM, deterministic), then points sorted by (cluster, squared
+    coordinate) — at Gamma = 0 the GW cost depends on the points only through
+    (s_i - t_j)^2, and the order keeps that band contiguous — or by (cluster,
+    Morton code of the first coordinates) without one."""
     x = points.to(torch.float64).contiguous()
     n, d = x.shape
     k = max(1, min(k, n))
@@ -157,7 +160,7 @@ def cluster_order(points: torch.Tensor, k: int = 64, sweeps: int = 8, seed: int 
         centers = torch.where(keep[:, None], sums / counts.clamp_min(1.0)[:, None], centers).contiguous()
     call("cntgw_km_assign", x.data_ptr(), n, d, centers.data_ptr(), k, assign.data_ptr(),
          own.data_ptr(), _stream())
-    fine = locality_order(x[:, : min(d, 3)])
+    fine = locality_order(x[:, : min(d, 3)]) if sq is None else torch.sort(sq, stable=True).indices
     rank = torch.empty_like(fine)
     rank[fine] = torch.arange(n, device=x.device)
     return torch.sort(assign * n + rank, stable=True).indices
@@ -170,7 +173,7 @@ def side_order(feat: torch.Tensor, sq: torch.Tensor | None) -> torch.Tensor:
     real = int((feat.abs().amax(0) > 0).sum()) if feat.numel() else 0
     if real <= 3 or feat.shape[1] not in (4, 8, 16, 32, 64):
         return locality_order(feat if sq is None else torch.cat([feat, sq[:, None]], 1))
-    return cluster_order(feat)
+    return cluster_order(feat, sq)
 
 
 def _tile_radii(pts: torch.Tensor, order: torch.Tensor, tile: int) -> torch.Tensor:

@@ -215,8 +215,8 @@ class _GwDevice:
             cols_feat = torch.zeros(self.m, self.kd, dtype=torch.float64, device=device)
         # locality orders of the point clouds (CNTGW_F32C tiles); the Gamma-dependent
         # features stay coherent along them (|Gamma dY| <= |Gamma| |dY|)
-        self.src = engine.Side(rows_feat, self.sx, self.a, order=engine.side_order(self.x, None))
-        self.tgt = engine.Side(cols_feat, self.ty, self.b, order=engine.side_order(self.y, None))
+        self.src = engine.Side(rows_feat, self.sx, self.a, order=self._order(self.x, self.sx))
+        self.tgt = engine.Side(cols_feat, self.ty, self.b, order=self._order(self.y, self.ty))
         self.fwd = engine.HalfUpdate(self.src, self.tgt, True)
         self.bwd = engine.HalfUpdate(self.tgt, self.src, True)
         self.loop = engine.SinkhornLoop(self.fwd, self.bwd, self.a, self.b, device, comm=self.comm)
@@ -235,6 +235,16 @@ class _GwDevice:
                   int(LIB.cntgw_outer_reduce_workspace(self.m, 1, 1)))
         self.ws_outer = torch.empty(ows, dtype=torch.uint8, device=device)
         self.prec = F32
+
+    @staticmethod
+    def _order(pts: torch.Tensor, sq: torch.Tensor) -> torch.Tensor:
+        """Locality order of a point cloud for the block-sparse paths: Morton
+        codes of low-dimensional points (CNTGW_F32C tiles; the Gamma-dependent
+        features stay coherent along them, |Gamma dY| <= |Gamma| |dY|), a
+        k-means order by (cluster, s) above (CNTGW_F64S)."""
+        if pts.shape[1] <= 3 or pts.shape[1] not in (4, 8, 16, 32, 64):
+            return engine.locality_order(pts)
+        return engine.cluster_order(pts, sq)
 
     # -- K5 -----------------------------------------------------------------
     def set_gamma(self, gamma: np.ndarray):
