@@ -223,7 +223,7 @@ size_t ctr_plan_bytes(const KernelPick& k, int64_t n, int64_t m) {
 // Measured plan of the CNTGW_F64S kernel: tmin [n][stages] fp32, need
 // [row tiles][stages] bytes, c at the last plan [mpad] fp64, CtrPlanKey.
 struct F64sPlanLayout {
-  size_t tmin, need, cplan, range, total;
+  size_t tmin, need, cplan, range, gmin, tstar, total;
   int stages;
   int64_t row_tiles;
 };
@@ -237,7 +237,9 @@ F64sPlanLayout f64s_layout(const KernelPick& k, int64_t n, int64_t m) {
   l.need = align256((size_t)l.row_tiles * l.stages);
   l.cplan = align256(sizeof(double) * (size_t)mpad);
   l.range = align256(sizeof(double2) * (size_t)l.stages);
-  l.total = l.tmin + l.need + l.cplan + l.range + 256;  // + CtrPlanKey, flag, counter
+  l.gmin = align256(sizeof(float) * (size_t)l.row_tiles * l.stages);
+  l.tstar = align256(sizeof(int) * (size_t)n);
+  l.total = l.tmin + l.need + l.cplan + l.range + l.gmin + l.tstar + 256;  // + CtrPlanKey, flag, counter
   return l;
 }
 
@@ -247,6 +249,8 @@ struct F64sPlan {
   uint8_t* need;
   double* c_plan;
   double2* range;
+  float* gmin;
+  int* tstar;
   CtrPlanKey* key;
   int* flag;
   int* counter;
@@ -259,7 +263,9 @@ F64sPlan f64s_plan(void* base_v, const F64sPlanLayout& l) {
   p.need = reinterpret_cast<uint8_t*>(base + l.tmin);
   p.c_plan = reinterpret_cast<double*>(base + l.tmin + l.need);
   p.range = reinterpret_cast<double2*>(base + l.tmin + l.need + l.cplan);
-  p.key = reinterpret_cast<CtrPlanKey*>(base + l.tmin + l.need + l.cplan + l.range);
+  p.gmin = reinterpret_cast<float*>(base + l.tmin + l.need + l.cplan + l.range);
+  p.tstar = reinterpret_cast<int*>(base + l.tmin + l.need + l.cplan + l.range + l.gmin);
+  p.key = reinterpret_cast<CtrPlanKey*>(base + l.tmin + l.need + l.cplan + l.range + l.gmin + l.tstar);
   p.flag = &p.key->replan;
   p.counter = reinterpret_cast<int*>(reinterpret_cast<char*>(p.key) + 128);
   p.next_measure = p.counter + 1;
@@ -279,8 +285,8 @@ int f64s_revote(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl
                                                         pl.flag);
   const char* te = getenv("CNTGW_CTR_SKIP_T");
   const double T = te ? atof(te) : 64.0;
-  f64s_vote_kernel<<<(unsigned)l.row_tiles, 256, sizeof(double) * k.cta_rows, s>>>(
-      pl.flag, pl.tmin, pl.range, n, l.stages, k.cta_rows, T, pl.need, pl.counter);
+  f64s_vote_kernel<<<(unsigned)l.row_tiles, 256, 0, s>>>(pl.flag, pl.gmin, pl.tstar, pl.range, n, l.stages,
+                                                         k.cta_rows, T, pl.need, pl.counter);
   const char* fe = getenv("CNTGW_F64S_REMEASURE");
   const double frac = fe ? atof(fe) : 0.25;
   f64s_decide_kernel<<<1, 1, 0, s>>>(st, pl.flag, pl.counter, pl.next_measure, l.row_tiles * (int64_t)l.stages,
@@ -818,6 +824,8 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
       return fail(CNTGW_ECUDA, "softmin f64s launch: %s", cudaGetErrorString(e2));
     }
     const int64_t mpad = (m + kColTile - 1) / kColTile * kColTile;
+    f64s_reduce_kernel<<<(unsigned)fl.row_tiles, 256, sizeof(double) * k.cta_rows, s>>>(
+        pl.flag, pl.tmin, n, fl.stages, k.cta_rows, pl.gmin, pl.tstar);
     f64s_commit_kernel<<<1, 1024, 0, s>>>(pl.flag, st, rec, cntgw_col_stride(CNTGW_F64S, kd, sq_flag),
                                           kd + (sq_flag ? 1 : 0), mpad, pl.c_plan, pl.key, row_feat, col_rec, n, m,
                                           pl.next_measure);

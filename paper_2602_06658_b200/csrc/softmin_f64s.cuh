@@ -60,14 +60,16 @@ __global__ void f64s_prep_rows_kernel(int kd, int sq_flag, const double* feat, i
 }
 
 // ---- the measured plan, re-voted every sweep ---------------------------------
-// State (workspace, f64s_layout): tmin[n][stages] — each row's minimum q over
-// each stage at the last MEASURED sweep — and c_plan, the column constants
-// -beta_j at that sweep. Every later sweep sees column shifts d_j = c_j -
-// c_plan_j; with [dmin_t, dmax_t] their range over stage t, the current
-//   stage minimum >= tmin[i][t] + dmin_t,
-//   row minimum   <= U_i = min_t (tmin[i][t] + dmax_t),
-// so a stage with tmin[i][t] + dmin_t > U_i + T for every row of a group
-// holds only terms below 2^-T of each row's maximum and is skipped. Uniform
+// State (workspace, f64s_layout): from the last MEASURED sweep, each row's
+// minimum q over each stage (tmin[n][stages], reduced right away to gmin =
+// per (row group, stage) the smallest tmin[i][t] - Mq_i, and t*_i = the stage
+// holding row i's minimum Mq_i), and c_plan, the column constants -beta_j at
+// that sweep. Every later sweep sees column shifts d_j = c_j - c_plan_j; with
+// [dmin_t, dmax_t] their range over stage t, for every row i of group g
+//   stage-t minimum >= Mq_i + gmin[g][t] + dmin_t,
+//   row minimum     <= Mq_i + dmax_{t*_i},
+// so a stage with gmin[g][t] + dmin_t > max_i dmax_{t*_i} + T holds only
+// terms below 2^-T of each of the group's rows' maxima and is skipped. Uniform
 // drifts cancel exactly, and per-stage ranges stay narrow while the global
 // spread of the shifts is large (a stage is 64-256 columns of one cluster).
 // A sweep measures anew (dense, tmin rewritten) on the first sweep of a
@@ -124,38 +126,89 @@ __global__ void __launch_bounds__(128) f64s_shift_kernel(const double* rec, int 
   }
 }
 
-// One block per row group of `grows` rows (skipped on a measuring sweep): the
-// rows' upper bounds U_i, then per stage an OR over the group's rows of
-// "tmin + dmin <= U + T" (NaN keeps the stage); counts the needed pairs.
-__global__ void __launch_bounds__(256) f64s_vote_kernel(const int* flag, const float* tmin,
-                                                        const double2* range, int64_t n, int stages, int grows,
-                                                        double T, uint8_t* need, int* counter) {
-  if (*flag) return;
-  extern __shared__ double ub[];  // [grows]
+// After a measuring sweep (one block per row group of `grows` rows): each
+// row's minimum Mq_i and argmin stage t*_i over the stage minima, and per
+// (group, stage) the smallest relative minimum gmin = min_i (tmin[i][t] -
+// Mq_i) (rounded down). The per-sweep re-vote reads only gmin and t*, not the
+// [n][stages] tmin (16 GB at N = M = 2^20).
+__global__ void __launch_bounds__(256) f64s_reduce_kernel(const int* flag, const float* tmin, int64_t n,
+                                                          int stages, int grows, float* gmin, int* tstar) {
+  if (!*flag) return;
+  extern __shared__ double rmin[];  // [grows]
   const int64_t r0 = (int64_t)blockIdx.x * grows;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int r = warp; r < grows; r += nw) {
-    double u = CUDART_INF;
+    float mn = CUDART_INF_F;
+    int at = 0;
     if (r0 + r < n)
-      for (int t = lane; t < stages; t += 32) u = fmin(u, (double)tmin[(r0 + r) * stages + t] + range[t].y);
+      for (int t = lane; t < stages; t += 32) {
+        const float v = tmin[(r0 + r) * stages + t];
+        if (v < mn) {
+          mn = v;
+          at = t;
+        }
+      }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) u = fmin(u, __shfl_xor_sync(0xffffffffu, u, o));
-    // tmin is rounded down (at most 2^-23 relative): widen the upper bound
-    if (lane == 0) ub[r] = u + fabs(u) * 0x1p-21;
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, mn, o);
+      const int a2 = __shfl_xor_sync(0xffffffffu, at, o);
+      if (m2 < mn || (m2 == mn && a2 < at)) {
+        mn = m2;
+        at = a2;
+      }
+    }
+    if (lane == 0) {
+      rmin[r] = mn;
+      if (r0 + r < n) tstar[r0 + r] = at;
+    }
   }
   __syncthreads();
+  // the stage minima were rounded down to fp32: the rows' true minima can sit
+  // up to an ulp of |Mq| above rmin, so gmin is lowered by two ulps of the
+  // group's largest |Mq| (keeps every bound of the vote conservative)
+  double amax = 0.0;
+  for (int r = 0; r < grows && r0 + r < n; ++r)
+    if (fabs(rmin[r]) < CUDART_INF) amax = fmax(amax, fabs(rmin[r]));
+  const double allow = amax * 0x1p-22;
+  for (int t = threadIdx.x; t < stages; t += blockDim.x) {
+    double g = CUDART_INF;
+    for (int r = 0; r < grows && r0 + r < n; ++r)
+      g = fmin(g, (double)tmin[(r0 + r) * stages + t] - rmin[r]);  // (inf - inf: an empty row, NaN dropped)
+    gmin[(int64_t)blockIdx.x * stages + t] = __double2float_rd(g - allow);
+  }
+}
+
+// One block per row group (skipped on a measuring sweep). For a row i of the
+// group, its current stage-t minimum is >= Mq_i + gmin[g][t] + dmin_t and
+// its current row minimum <= Mq_i + dmax_{t*_i} (the stage that held its
+// minimum at the measurement), so stage t can hold a term within T of the
+// row's maximum only if gmin[g][t] + dmin_t <= D_g + T, D_g = max over the
+// group's rows of dmax_{t*_i}. Counts the needed pairs.
+__global__ void __launch_bounds__(256) f64s_vote_kernel(const int* flag, const float* gmin, const int* tstar,
+                                                        const double2* range, int64_t n, int stages, int grows,
+                                                        double T, uint8_t* need, int* counter) {
+  if (*flag) return;
+  __shared__ double dg_s[8];
+  const int64_t r0 = (int64_t)blockIdx.x * grows;
+  double dg = -CUDART_INF;
+  for (int r = threadIdx.x; r < grows; r += blockDim.x)
+    if (r0 + r < n) dg = fmax(dg, range[tstar[r0 + r]].y);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dg = fmax(dg, __shfl_xor_sync(0xffffffffu, dg, o));
+  if ((threadIdx.x & 31) == 0) dg_s[threadIdx.x >> 5] = dg;
+  __syncthreads();
+  dg = dg_s[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) dg = fmax(dg, dg_s[w]);
+  const double lim = dg + T;  // (gmin already carries the fp32 rounding allowance)
   int cnt = 0;
   for (int t = threadIdx.x; t < stages; t += blockDim.x) {
-    uint8_t v = 0;
-    const double dmin = range[t].x;
-    for (int r = 0; r < grows && r0 + r < n && !v; ++r)
-      v = !((double)tmin[(r0 + r) * stages + t] + dmin > ub[r] + T) ? 1 : 0;
+    const uint8_t v = !((double)gmin[(int64_t)blockIdx.x * stages + t] + range[t].x > lim) ? 1 : 0;
     need[(int64_t)blockIdx.x * stages + t] = v;
     cnt += v;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  if (lane == 0 && cnt) atomicAdd(counter, cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(counter, cnt);
 }
 
 // (1 thread) measure anew when the re-vote kept too much, and on a geometric
@@ -200,6 +253,54 @@ __global__ void __launch_bounds__(1024) f64s_commit_kernel(const int* flag, cons
     key->cols = cols;
     key->n = n;
     key->m = m;
+  }
+}
+
+// dmma_consume plus the step's minimum q per row group, tracked on the fp32
+// exponent arguments x = mq - q (FMNMX on the ALU, not a DMNMX per term on
+// the FP64 pipe): tm = min(tm, mq - max x), one fp64 op per row group and
+// step. The fp32 argument (truncated, ~2^-18 relative at 32-48 log2 units)
+// is exact enough for a plan whose margins are 64 log2 units.
+template <int RG, int NT>
+__device__ __forceinline__ void dmma_consume_min(const double (&q)[RG][NT][2], double (&mq)[RG], double (&S)[RG],
+                                                 float (&T)[RG], double (&tm)[RG]) {
+  float gsum[RG], xmax[RG];
+#pragma unroll
+  for (int rg = 0; rg < RG; ++rg) {
+    float2 acc = f2(0.f, 0.f);
+    float xm = -CUDART_INF_F;
+#pragma unroll
+    for (int u = 0; u < NT; ++u) {
+      const float2 x = f2(f64_to_f32_fast(mq[rg] - q[rg][u][0]), f64_to_f32_fast(mq[rg] - q[rg][u][1]));
+      xm = fmaxf(xm, fmaxf(x.x, x.y));
+      acc = add2(acc, f2(ex2(x.x), ex2(x.y)));
+    }
+    gsum[rg] = acc.x + acc.y;
+    xmax[rg] = xm;
+  }
+#pragma unroll
+  for (int rg = 0; rg < RG; ++rg) {
+    if (!(gsum[rg] <= kRebaseF64)) {  // rare: rebase kRefOffset above the group minimum
+      double qmin = q[rg][0][0];
+#pragma unroll
+      for (int u = 0; u < NT; ++u) qmin = fmin(qmin, fmin(q[rg][u][0], q[rg][u][1]));
+      const double ref = qmin + kRefOffset;
+      if (ref < mq[rg]) {
+        const double sc = exp2(ref - mq[rg]);
+        S[rg] *= sc;
+        T[rg] *= (float)sc;
+        mq[rg] = ref;
+      }
+      float r = 0.f;
+#pragma unroll
+      for (int u = 0; u < NT; ++u)
+        r += ex2(f64_to_f32_fast(mq[rg] - q[rg][u][0])) + ex2(f64_to_f32_fast(mq[rg] - q[rg][u][1]));
+      gsum[rg] = r;
+      tm[rg] = fmin(tm[rg], qmin);
+    } else {
+      tm[rg] = fmin(tm[rg], mq[rg] - (double)xmax[rg]);
+    }
+    T[rg] += gsum[rg];
   }
 }
 
@@ -294,13 +395,10 @@ __global__ void __launch_bounds__(128, MINB) softmin_f64s_kernel(const SoftminAr
     for (int ct = 0; ct < TILE; ct += 8 * NT) {
       double q[RG][NT][2];
       dmma_scores<KD, SQ, RG, NT, KS>(tile, ct, lr, lk, afr, q);
-      if (replan) {
-#pragma unroll
-        for (int rg = 0; rg < RG; ++rg)
-#pragma unroll
-          for (int u = 0; u < NT; ++u) tm[rg] = fmin(tm[rg], fmin(q[rg][u][0], q[rg][u][1]));
-      }
-      dmma_consume<RG, NT>(q, mq, S, T);
+      if (replan)  // (the measuring sweep: stage minima ride on the exponent arguments)
+        dmma_consume_min<RG, NT>(q, mq, S, T, tm);
+      else
+        dmma_consume<RG, NT>(q, mq, S, T);
     }
 #pragma unroll
     for (int rg = 0; rg < RG; ++rg) S[rg] += f32_to_f64_alu(T[rg]);
@@ -311,7 +409,8 @@ __global__ void __launch_bounds__(128, MINB) softmin_f64s_kernel(const SoftminAr
         v = fmin(v, __shfl_xor_sync(0xffffffffu, v, 1));
         v = fmin(v, __shfl_xor_sync(0xffffffffu, v, 2));
         const int64_t i = wrow + 8 * rg + lr;
-        if (lk == 0 && i < a.n) p.tmin[i * p.stages + t0 + list[k]] = __double2float_rd(v);
+        if (lk == 0 && i < a.n)  // (- 2^-10: the fp32 exponent arguments were truncated)
+          p.tmin[i * p.stages + t0 + list[k]] = __double2float_rd(v - 0x1p-10);
       }
     }
     ring.release(k);

@@ -256,11 +256,13 @@ def choose_precision(scale: float, kd: int = 0, sq: bool = True, ctr_deferred=No
     if forced in ("f32c", "ctr"):
         return F32C if ctr_supported(kd, sq) else F64
     if scale >= F32_EXPONENT_LIMIT:
+        # large cold problems: fp64 with the measured block-sparse plan (C4 at
+        # 2^20: 79 s vs 157 s on the centred fp32 path, and fp64-exact terms)
+        if pairs >= F64S_MIN_PAIRS and os.environ.get("CNTGW_F64S", "1") != "0":
+            return F64S
         if (ctr_deferred is not None and ctr_supported(kd, sq)
                 and os.environ.get("CNTGW_CTR", "1") != "0" and ctr_deferred() <= CTR_MAX_DEFERRED):
             return F32C
-        if pairs >= F64S_MIN_PAIRS and os.environ.get("CNTGW_F64S", "1") != "0":
-            return F64S
         return F64
     return TF32X3 if tc_supported(kd, sq) else F32
 

@@ -153,12 +153,23 @@ def test_c4_full_size_argmax(c4_state):
 
 
 def test_c4_full_size_half_updates_vs_oracle(c4_state):
-    """C4 at N=M=2^20 on the automatic path: the block-sparse centred fp32
-    kernel (CNTGW_F32C) with its plan reused across the warm sweeps."""
-    from paper_2602_06658_b200._native import F32C
+    """C4 at N=M=2^20 on the automatic path: fp64 DMMA with the measured
+    block-sparse plan (CNTGW_F64S), re-voted across the warm sweeps."""
+    from paper_2602_06658_b200._native import F64S
 
     src, tgt, st = c4_state
     prec = _check_half_updates(st, src, tgt, n_rows=384, n_cols=384, seed=4)
+    assert prec == F64S
+
+
+def test_c4_full_size_centred_path_vs_oracle(c4_state, monkeypatch):
+    """The same warm C4 pair on the block-sparse centred fp32 kernel
+    (CNTGW_F32C, geometric plan reused across sweeps)."""
+    from paper_2602_06658_b200._native import F32C
+
+    monkeypatch.setenv("CNTGW_PRECISION", "f32c")
+    src, tgt, st = c4_state
+    prec = _check_half_updates(st, src, tgt, n_rows=256, n_cols=256, seed=14)
     assert prec == F32C
 
 

@@ -12,18 +12,20 @@ from paper_2602_06658_b200._native import F64S, call
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 18
 outer = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 sweeps = int(sys.argv[3]) if len(sys.argv) > 3 else 60
+law = sys.argv[4] if len(sys.argv) > 4 else "c5"
 torch.cuda.set_device(0)
 os.environ["CNTGW_PRECISION"] = "f64s"
-pc = configs.c5(seed=0, n=n)
-src = P.embed_measure(P.DiscreteMeasure(pc.x, pc.a), P.CostSpec("sq_euclidean"), dim=64)
-tgt = P.embed_measure(P.DiscreteMeasure(pc.y, pc.b), P.CostSpec("sq_euclidean"), dim=32)
-st = solvers._CntGwState(src, tgt, P.make_config(configs.C5_EPS, n_inner=50, max_outer=outer + 1))
+pc = configs.GENERATORS[law.upper()](seed=0, n=n)
+EPS = configs.C5_EPS if law == "c5" else configs.C4_EPS
+src = P.embed_measure(P.DiscreteMeasure(pc.x, pc.a), P.CostSpec("sq_euclidean"), dim=pc.x.shape[1])
+tgt = P.embed_measure(P.DiscreteMeasure(pc.y, pc.b), P.CostSpec("sq_euclidean"), dim=pc.y.shape[1])
+st = solvers._CntGwState(src, tgt, P.make_config(EPS, n_inner=50, max_outer=outer + 1))
 for _ in range(outer):
     st.step()
 dev = st.dev
 dev.set_gamma(st.gamma)
-dev.choose_precision(st.f, st.g, configs.C5_EPS / 8)
-eps = configs.C5_EPS / 8
+dev.choose_precision(st.f, st.g, EPS / 8)
+eps = EPS / 8
 loop = dev.loop
 loop.state.init(eps, None, None, sweeps + 5, "symmetrized")
 out = torch.zeros(3, dtype=torch.int64, device="cuda")
