@@ -524,7 +524,9 @@ def gw_solve_block(args, info, dev):
         "config": f"C4 (N=M={n}, d=3, eps=0.01, {outer} outer x {inner} sweeps)",
         "seconds": secs, "n_gpus": info.world, "objectives": objs, "marginal_errs": errs,
         "precision_path": {0: "fp32", 1: "fp64 DMMA", 2: "tcgen05 3xTF32",
-                           3: "block-sparse centred fp32 (F32C)"}[int(st.dev.prec)],
+                           3: "block-sparse centred fp32 (F32C)",
+                           4: "fp64 DMMA + measured block-sparse plan (F64S)"}.get(int(st.dev.prec),
+                                                                                   str(int(st.dev.prec))),
         "nm_pairs_per_s": passes * float(n) * n / secs,
         "timing": "CUDA events around state setup + all outer steps (host arrays in), max over ranks",
         "clocks": clocks.summary(),
