@@ -131,29 +131,30 @@ def test_partial_lse_c2_shape_two_shards(cuda, prec_name):
     assert np.abs(got[cols] - want).max() / np.abs(want).max() < 1e-5
 
 
-@pytest.mark.parametrize("prec_name", ["dmma", "f32c"])
+@pytest.mark.parametrize("prec_name", ["dmma", "f64s", "f32c"])
 def test_partial_lse_c5_and_c4_shapes_two_shards(cuda, prec_name, monkeypatch):
     """C5 shape (E-side projection: 32 dot features + the squared coordinate)
-    on the fp64 DMMA kernel, and the C4 shape (3 + sq) on the centred kernel
-    (partials scattered back to the caller's order), cold regime: sharded
-    g-update = the oracle on sampled columns."""
+    on the fp64 DMMA kernel and on CNTGW_F64S (ordered rows, measured plan),
+    and the C4 shape (3 + sq) on the centred kernel (partials scattered back
+    to the caller's order), cold regime: sharded g-update = the oracle on
+    sampled columns."""
     from oracle import cntgw_oracle as O
-    from paper_2602_06658_b200._native import F32C, F64
+    from paper_2602_06658_b200._native import F32C, F64, F64S
 
     rng = np.random.default_rng(5)
     n = m = 1 << 14
-    k = 32 if prec_name == "dmma" else 3
+    k = 3 if prec_name == "f32c" else 32
     cx = rng.standard_normal((8, k)) * 2.0
     x = cx[rng.integers(0, 8, n)] + rng.standard_normal((n, k)) * 0.6
     z = cx[rng.integers(0, 8, m)] + rng.standard_normal((m, k)) * 0.6
     xs, zs = 0.5 * (x * x).sum(1), 0.5 * (z * z).sum(1)
     a = np.full(n, 1.0 / n)
     b = np.full(m, 1.0 / m)
-    eps = 2.5e-3 if prec_name == "dmma" else 1.25e-3
+    eps = 1.25e-3 if prec_name == "f32c" else 2.5e-3
     row_sep, col_sep = (x * x).sum(1), (z * z).sum(1)
     f = rng.standard_normal(n) * 3.0 + row_sep + xs * xs
     monkeypatch.setenv("CNTGW_F64_DMMA", "1")
-    prec = F64 if prec_name == "dmma" else F32C
+    prec = {"dmma": F64, "f64s": F64S, "f32c": F32C}[prec_name]
     got = _sharded_g_update(prec, x, xs, z, zs, a, b, f, row_sep, eps) + col_sep
     cols = np.sort(rng.choice(m, 96, replace=False))
     cost = O.SqEuclid(np.column_stack([x, xs]), np.column_stack([z, zs]))
