@@ -356,6 +356,51 @@ int cntgw_graph_end(void* stream, void** exec_out);
 int cntgw_graph_launch(void* exec, void* stream);
 int cntgw_graph_destroy(void* exec);
 
+/* ---- solve-level API: the CNT-GW feature-space solve (solvers.py:628-632) ---
+ * A native driver over the entry points above, for callers without the Python
+ * package. One handle per device and problem; every buffer is allocated by
+ * cntgw_solver_create (the only allocating call of the library) and freed by
+ * cntgw_solver_destroy. cntgw_solver_run captures the whole solve — outer loop
+ * (stop rule, 5-increase divergence guard), Sinkhorn loops at eps/8 (fixed
+ * budget or threshold), plan passes — as ONE CUDA graph and launches it. */
+typedef struct cntgw_solve_config {
+  double eps;          /* EgwConfig.eps (the Sinkhorn loops run at eps/8)           */
+  int mode;            /* 1 symmetrized (default), 0 standard                        */
+  int n_inner;         /* fixed sweep budget (threshold == 0)                         */
+  double threshold;    /* weighted-gap tolerance, 0 for a fixed budget              */
+  int max_inner;       /* sweep cap in threshold mode                                 */
+  double anneal_from;  /* SinkhornConfig.anneal_from in eps/8 units, 0 = none         */
+  int max_outer;       /* EgwConfig.max_outer                                         */
+  double delta_outer;  /* EgwConfig.delta_outer                                       */
+  int precision;       /* half-update path: CNTGW_F32, CNTGW_F64 or CNTGW_F64S        */
+} cntgw_solve_config;
+typedef struct cntgw_solver cntgw_solver;
+/* x: n x d and y: m x e centred features, a, b weights (device fp64, caller-
+ * owned, alive until destroy). order_x / order_y: locality orders for
+ * CNTGW_F64S (NULL = identity). comm: NULL, or a communicator whose ranks each
+ * pass their row shard (n rows of n_total; n_rows_max = the largest shard). */
+int cntgw_solver_create(cntgw_solver** out, const double* x, int64_t n, int d, const double* y, int64_t m, int e,
+                        const double* a, const double* b, const int64_t* order_x, const int64_t* order_y,
+                        const cntgw_solve_config* cfg, cntgw_comm* comm, int64_t n_rows_max, void* stream);
+int cntgw_solver_destroy(cntgw_solver* solver);
+/* f~ = s^2, g~ = t^2: the interaction potentials of the default init (solvers.py:297-301). */
+int cntgw_solver_init_potentials(cntgw_solver* solver, double* f, double* g, void* stream);
+/* One solve. constant: the loss constant (cntgw_gw_constant). gamma: d*e device
+ * fp64, in Gamma_0, out Gamma_{t+1} = EgwResult.gamma; gamma_prev: out Gamma_t
+ * (the returned coupling's operator); f, g: device interaction potentials, in
+ * the warm start, out the coupling's. trace_host: 5*max_outer doubles, rows
+ * [objective, gamma_delta, marginal_err, inner_iters, elapsed_s];
+ * status_host[4] = {outer steps, converged, error (SolverError), sweeps applied}. */
+int cntgw_solver_run(cntgw_solver* solver, double constant, double* gamma, double* gamma_prev, double* f, double* g,
+                     double* trace_host, int* status_host, void* stream);
+/* Outputs of the last plan pass copied into caller device buffers (each
+ * nullable): row masses (n fp64), argmax plan indices (n int64); eps_eff (host). */
+int cntgw_solver_results(const cntgw_solver* solver, double* row_mass, int64_t* argmax, double* eps_eff,
+                         void* stream);
+/* The loss constant C = Q(X) + Q(Y) - 4 T_X T_Y (divergence.py:28-47) in closed form. */
+int cntgw_gw_constant(const double* x, int64_t n, int d, const double* a, const double* y, int64_t m, int e,
+                      const double* b, double* out_host, void* stream);
+
 /* ---- kernel PCA: matrix-free cost products (kernels.py:149-345) --------
  * out (n x bcols) = C V with C_ij = c(x_i, x_j) evaluated on the fly in fp64
  * from sq = |x_i|^2 + |x_j|^2 - 2 x_i.x_j clipped at 0 (sqn = |x|^2), c_ii = 0;

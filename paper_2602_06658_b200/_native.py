@@ -32,6 +32,16 @@ class SweepStateStruct(ctypes.Structure):
     ]
 
 
+class SolveConfigStruct(ctypes.Structure):
+    """Host mirror of ``cntgw_solve_config`` (include/cntgw_b200.h)."""
+
+    _fields_ = [
+        ("eps", c_double), ("mode", c_int), ("n_inner", c_int), ("threshold", c_double),
+        ("max_inner", c_int), ("anneal_from", c_double), ("max_outer", c_int),
+        ("delta_outer", c_double), ("precision", c_int),
+    ]
+
+
 class OuterStateStruct(ctypes.Structure):
     """Host mirror of ``cntgw_outer_state`` (include/cntgw_b200.h)."""
 
@@ -84,6 +94,13 @@ SIGNATURES = {
     "cntgw_comm_allreduce": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp]),
     "cntgw_lse_rescale": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
     "cntgw_comm_combine_lse": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "cntgw_solver_create": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_vp,
+                                    c_vp, c_vp, c_i64, c_vp]),
+    "cntgw_solver_destroy": (c_int, [c_vp]),
+    "cntgw_solver_init_potentials": (c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "cntgw_solver_run": (c_int, [c_vp, c_double, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "cntgw_solver_results": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "cntgw_gw_constant": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_i64, c_int, c_vp, c_vp, c_vp]),
     "cntgw_f64s_rows_bytes": (c_size_t, [c_i64, c_int]),
     "cntgw_f64s_plan_density": (c_int, [c_int, c_int, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "cntgw_prep_rows_f64s": (c_int, [c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp]),
