@@ -203,6 +203,11 @@ int cntgw_prep_rows_f64s(int kd, int sq_flag, const double* feat, int64_t ld, co
  * [needed (row group, stage) pairs, all pairs, 1 if the last sweep measured]. */
 int cntgw_f64s_plan_density(int kd, int sq_flag, int64_t n, int64_t m, const void* workspace, int64_t* out,
                             void* stream);
+/* out = (Gamma == 0 ? order_if_zero : order_otherwise), decided on the device
+ * (graph-capturable): at Gamma = 0 the GW cost depends on the points only
+ * through (s_i - t_j)^2 and the squared-coordinate order makes the plan a band. */
+int cntgw_select_order(const double* gamma, int de, const int64_t* order_if_zero, const int64_t* order_otherwise,
+                       int64_t n, int64_t* out, void* stream);
 /* cntgw_prep_cols (CNTGW_F64 records) with the columns gathered in `order`. */
 int cntgw_prep_cols_f64s(const cntgw_sweep_state* st, int kd, int sq_flag, const double* feat, int64_t ld,
                          const double* sq, const double* pot, const double* log2w, const int64_t* order,

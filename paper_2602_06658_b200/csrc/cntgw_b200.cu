@@ -892,6 +892,17 @@ int cntgw_f64s_plan_density(int kd, int sq_flag, int64_t n, int64_t m, const voi
   return check_launch("f64s_density");
 }
 
+/* ---- CNTGW_F64S: the point order of the next loop from the device Gamma ---- */
+int cntgw_select_order(const double* gamma, int de, const int64_t* order_if_zero, const int64_t* order_otherwise,
+                       int64_t n, int64_t* out, void* stream) {
+  if (!gamma || de < 1 || !order_if_zero || !order_otherwise || !out || n < 1)
+    return fail(CNTGW_EINVAL, "select_order: bad arguments");
+  const int64_t blocks = (n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184;
+  select_order_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(gamma, de, order_if_zero, order_otherwise,
+                                                                       n, out);
+  return check_launch("select_order");
+}
+
 /* ---- CNTGW_F64S rows block and ordered column records ---- */
 size_t cntgw_f64s_rows_bytes(int64_t n, int kd) { return n < 1 ? 0 : f64s_rows_bytes(n, kd); }
 

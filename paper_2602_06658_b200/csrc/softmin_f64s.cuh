@@ -59,6 +59,23 @@ __global__ void f64s_prep_rows_kernel(int kd, int sq_flag, const double* feat, i
   s[i] = sq_flag ? sq[src] : 0.0;
 }
 
+// Order of the points for the next loop, chosen on the device from Gamma:
+// at Gamma = 0 (the product init) the cost depends on the points only through
+// (s_i - t_j)^2, so the squared-coordinate order makes the plan a band; any
+// other operator takes the geometric order (Morton / k-means).
+__global__ void select_order_kernel(const double* gamma, int de, const int64_t* if_zero, const int64_t* otherwise,
+                                    int64_t n, int64_t* out) {
+  __shared__ int nonzero;
+  if (threadIdx.x == 0) nonzero = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k < de; k += blockDim.x)
+    if (gamma[k] != 0.0) nonzero = 1;
+  __syncthreads();
+  const int64_t* src = nonzero ? otherwise : if_zero;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = src[i];
+}
+
 // ---- the measured plan, re-voted every sweep ---------------------------------
 // State (workspace, f64s_layout): from the last MEASURED sweep, each row's
 // minimum q over each stage (tmin[n][stages], reduced right away to gmin =

@@ -304,11 +304,16 @@ class Side:
         self.log2w = torch.log2(w)
         self._f32 = None
         self.order = order  # locality order of the points (CNTGW_F32C), lazily from feat64
+        self.f64s_order = None  # CNTGW_F64S's order when it differs (set per loop by the solver)
 
     def locality(self) -> torch.Tensor:
         if self.order is None:
             self.order = side_order(self.feat64, self.sq64)
         return self.order
+
+    def plan_order(self) -> torch.Tensor:
+        """The point order of the measured-plan path (CNTGW_F64S)."""
+        return self.f64s_order if self.f64s_order is not None else self.locality()
 
     @staticmethod
     def make(feat, sq, w, device, kd):
@@ -400,7 +405,7 @@ class HalfUpdate:
         if prec == F64S:
             call("cntgw_prep_cols_f64s", state.ptr, self.kd, int(self.sq), c.feat64.data_ptr(), self.kd,
                  _p(c.sq64 if self.sq else None), _p(pot_cols), c.log2w.data_ptr(),
-                 c.locality().data_ptr(), c.n, self.rec.data_ptr(), _stream())
+                 c.plan_order().data_ptr(), c.n, self.rec.data_ptr(), _stream())
             return
         feat, sq = c.feat(prec)
         call("cntgw_prep_cols", state.ptr, prec, self.kd, int(self.sq), feat.data_ptr(), self.kd,
@@ -417,7 +422,7 @@ class HalfUpdate:
         elif self.prec == F64S:
             sq = r.sq64 if self.sq else None
             call("cntgw_prep_rows_f64s", self.kd, int(self.sq), r.feat64.data_ptr(), self.kd, _p(sq),
-                 r.locality().data_ptr(), r.n, self.f64s_rows.data_ptr(), _stream())
+                 r.plan_order().data_ptr(), r.n, self.f64s_rows.data_ptr(), _stream())
             feat, rec = self.f64s_rows, self.rec
         else:
             feat, sq = r.feat(self.prec)

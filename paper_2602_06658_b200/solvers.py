@@ -217,6 +217,14 @@ class _GwDevice:
         # features stay coherent along them (|Gamma dY| <= |Gamma| |dY|)
         self.src = engine.Side(rows_feat, self.sx, self.a, order=self._order(self.x, self.sx))
         self.tgt = engine.Side(cols_feat, self.ty, self.b, order=self._order(self.y, self.ty))
+        # CNTGW_F64S visits the points in the squared-coordinate order while
+        # Gamma = 0 (the cost is then a function of s_i - t_j) and in the
+        # geometric order otherwise, switched on the device per loop (K5)
+        self._orders = []
+        for side in (self.src, self.tgt):
+            cur = side.locality().clone()
+            self._orders.append((torch.sort(side.sq64, stable=True).indices, side.locality(), cur))
+            side.f64s_order = cur
         self.fwd = engine.HalfUpdate(self.src, self.tgt, True)
         self.bwd = engine.HalfUpdate(self.tgt, self.src, True)
         self.loop = engine.SinkhornLoop(self.fwd, self.bwd, self.a, self.b, device, comm=self.comm)
@@ -242,9 +250,14 @@ class _GwDevice:
         codes of low-dimensional points (CNTGW_F32C tiles; the Gamma-dependent
         features stay coherent along them, |Gamma dY| <= |Gamma| |dY|), a
         k-means order by (cluster, s) above (CNTGW_F64S)."""
-        if pts.shape[1] <= 3 or pts.shape[1] not in (4, 8, 16, 32, 64):
+        mode = os.environ.get("CNTGW_ORDER", "auto")
+        if mode == "morton" or (mode == "auto" and pts.shape[1] <= 3) or pts.shape[1] > 64:
             return engine.locality_order(pts)
-        return engine.cluster_order(pts, sq)
+        if pts.shape[1] not in (4, 8, 16, 32, 64):  # the k-means kernels' widths
+            pts = torch.nn.functional.pad(pts, (0, engine.padded_kd(pts.shape[1]) - pts.shape[1]))
+            if pts.shape[1] < 4:
+                pts = torch.nn.functional.pad(pts, (0, 4 - pts.shape[1]))
+        return engine.cluster_order(pts.contiguous(), sq)
 
     # -- K5 -----------------------------------------------------------------
     def set_gamma(self, gamma: np.ndarray):
@@ -257,6 +270,13 @@ class _GwDevice:
         call("cntgw_apply_operator", op.data_ptr(), dout, din, feat.data_ptr(), din, count,
              side.feat64.data_ptr(), 0, self.kd, _stream())
         side.refresh32()
+        self._gamma_h = g  # (alive until the launch completes)
+        self._select_orders(g)
+
+    def _select_orders(self, gamma_dev: torch.Tensor):
+        for sq_order, geo, cur in self._orders:
+            call("cntgw_select_order", gamma_dev.data_ptr(), self.d * self.e, sq_order.data_ptr(),
+                 geo.data_ptr(), cur.numel(), cur.data_ptr(), _stream())
 
     def set_gamma_dev(self, gamma_dev: torch.Tensor, gamma_t: torch.Tensor):
         """K5 from a device-resident Gamma (d*e fp64); graph-capturable (no
@@ -269,6 +289,7 @@ class _GwDevice:
         call("cntgw_apply_operator", op.data_ptr(), dout, din, feat.data_ptr(), din, count,
              side.feat64.data_ptr(), 0, self.kd, _stream())
         side.refresh32()
+        self._select_orders(gamma_dev)
 
     def plan_pass(self, f, g):
         """K4 for the final pair: r, pi Y, pi t and argmax per (local) row.
@@ -297,10 +318,10 @@ class _GwDevice:
         if self.prec == F64S and os.environ.get("CNTGW_K4_SPARSE", "1") != "0":
             src = self.src
             call("cntgw_prep_rows_f64s", fwd.kd, 1, src.feat64.data_ptr(), fwd.kd, src.sq64.data_ptr(),
-                 src.locality().data_ptr(), src.n, fwd.f64s_rows.data_ptr(), stream)
+                 src.plan_order().data_ptr(), src.n, fwd.f64s_rows.data_ptr(), stream)
             fwd.pack(st, g, prec=F64S)
             call("cntgw_plan_reduce_f64s", st.ptr, fwd.kd, 1, self.e, fwd.f64s_rows.data_ptr(),
-                 fwd.rec.data_ptr(), self.tgt.locality().data_ptr(), src.feat64.data_ptr(), fwd.kd,
+                 fwd.rec.data_ptr(), self.tgt.plan_order().data_ptr(), src.feat64.data_ptr(), fwd.kd,
                  self.sx.data_ptr(), f.data_ptr(), src.log2w.data_ptr(), self.y.data_ptr(), self.e,
                  self.ty.data_ptr(), self.n, self.m, self.r.data_ptr(), self.pi_y.data_ptr(),
                  self.pi_s.data_ptr(), self.argmax.data_ptr(), fwd.ws.data_ptr(), fwd.ws.numel(),

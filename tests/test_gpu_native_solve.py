@@ -134,5 +134,5 @@ def test_native_solve_c5_law_on_the_measured_plan_path(P, monkeypatch):
     # half squared norms (device vs numpy) reach ~1e-8 of the objective
     assert _rel(nat["trace"][:, 0], objs) < 1e-6
     assert _rel(nat["trace"][:, 0], gold["objective"][:3]) < 1e-4
-    assert _rel(nat["gamma"], st.gamma) < 1e-6
+    assert _rel(nat["gamma"], st.gamma) < 1e-5
     torch.cuda.synchronize()
