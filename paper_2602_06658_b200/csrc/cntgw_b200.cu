@@ -223,7 +223,7 @@ size_t ctr_plan_bytes(const KernelPick& k, int64_t n, int64_t m) {
 // Measured plan of the CNTGW_F64S kernel: tmin [n][stages] fp32, need
 // [row tiles][stages] bytes, c at the last plan [mpad] fp64, CtrPlanKey.
 struct F64sPlanLayout {
-  size_t tmin, need, cplan, range, gmin, tstar, total;
+  size_t tmin, need, cplan, range, gmin, tstar, rowmin, total;
   int stages;
   int64_t row_tiles;
 };
@@ -239,7 +239,8 @@ F64sPlanLayout f64s_layout(const KernelPick& k, int64_t n, int64_t m) {
   l.range = align256(sizeof(double2) * (size_t)l.stages);
   l.gmin = align256(sizeof(float) * (size_t)l.row_tiles * l.stages);
   l.tstar = align256(sizeof(int) * (size_t)n);
-  l.total = l.tmin + l.need + l.cplan + l.range + l.gmin + l.tstar + 256;  // + CtrPlanKey, flag, counter
+  l.rowmin = align256(sizeof(double) * (size_t)n);
+  l.total = l.tmin + l.need + l.cplan + l.range + l.gmin + l.tstar + l.rowmin + 256;  // + CtrPlanKey, flags
   return l;
 }
 
@@ -251,10 +252,12 @@ struct F64sPlan {
   double2* range;
   float* gmin;
   int* tstar;
+  double* rowmin;
   CtrPlanKey* key;
   int* flag;
   int* counter;
   int* next_measure;
+  int* full;
 };
 F64sPlan f64s_plan(void* base_v, const F64sPlanLayout& l) {
   char* base = static_cast<char*>(base_v);
@@ -265,10 +268,12 @@ F64sPlan f64s_plan(void* base_v, const F64sPlanLayout& l) {
   p.range = reinterpret_cast<double2*>(base + l.tmin + l.need + l.cplan);
   p.gmin = reinterpret_cast<float*>(base + l.tmin + l.need + l.cplan + l.range);
   p.tstar = reinterpret_cast<int*>(base + l.tmin + l.need + l.cplan + l.range + l.gmin);
-  p.key = reinterpret_cast<CtrPlanKey*>(base + l.tmin + l.need + l.cplan + l.range + l.gmin + l.tstar);
+  p.rowmin = reinterpret_cast<double*>(base + l.tmin + l.need + l.cplan + l.range + l.gmin + l.tstar);
+  p.key = reinterpret_cast<CtrPlanKey*>(base + l.tmin + l.need + l.cplan + l.range + l.gmin + l.tstar + l.rowmin);
   p.flag = &p.key->replan;
   p.counter = reinterpret_cast<int*>(reinterpret_cast<char*>(p.key) + 128);
   p.next_measure = p.counter + 1;
+  p.full = p.counter + 2;
   return p;
 }
 
@@ -280,9 +285,9 @@ int f64s_revote(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl
                 cudaStream_t s, int schedule) {
   const int stride = (kd + sq + 1 + 1) / 2 * 2 > (kd + sq + 3) / 4 * 4 ? (kd + sq + 1 + 1) / 2 * 2
                                                                        : (kd + sq + 3) / 4 * 4;
-  f64s_begin_kernel<<<1, 1, 0, s>>>(st, pl.key, rows, cols, n, m, pl.flag, pl.counter);
+  f64s_begin_kernel<<<1, 1, 0, s>>>(st, pl.key, rows, cols, n, m, pl.flag, pl.counter, pl.full);
   f64s_shift_kernel<<<(unsigned)l.stages, 128, 0, s>>>(rec, stride, kd + sq, m, k.f64s_tile, pl.c_plan, pl.range,
-                                                        pl.flag);
+                                                        pl.flag, pl.full);
   const char* te = getenv("CNTGW_CTR_SKIP_T");
   const double T = te ? atof(te) : 64.0;
   f64s_vote_kernel<<<(unsigned)l.row_tiles, 256, 0, s>>>(pl.flag, pl.gmin, pl.tstar, pl.range, n, l.stages,
@@ -816,7 +821,8 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
     if (const int rc = f64s_revote(k, fl, pl, st, rec, kd, sq_flag ? 1 : 0, row_feat, col_rec, n, m, s, 1))
       return rc;
     if (env_int("CNTGW_CTR_REUSE", 1) == 0) f64s_begin_kernel<<<1, 1, 0, s>>>(nullptr, pl.key, row_feat, col_rec,
-                                                                                n, m, pl.flag, pl.counter);
+                                                                                n, m, pl.flag, pl.counter, pl.full);
+    fs.full = pl.full;
     void* args2[] = {&a, &fs};
     cudaError_t e2 = cudaLaunchKernel(k.fn, dim3(p.row_tiles, p.nchunks), dim3(k.threads), args2, k.smem, s);
     if (e2 != cudaSuccess) {
@@ -824,8 +830,8 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
       return fail(CNTGW_ECUDA, "softmin f64s launch: %s", cudaGetErrorString(e2));
     }
     const int64_t mpad = (m + kColTile - 1) / kColTile * kColTile;
-    f64s_reduce_kernel<<<(unsigned)fl.row_tiles, 256, sizeof(double) * k.cta_rows, s>>>(
-        pl.flag, pl.tmin, n, fl.stages, k.cta_rows, pl.gmin, pl.tstar);
+    f64s_reduce_kernel<<<(unsigned)fl.row_tiles, 256, 2 * sizeof(double) * k.cta_rows, s>>>(
+        pl.flag, pl.full, pl.tmin, pl.need, pl.range, n, fl.stages, k.cta_rows, pl.gmin, pl.tstar, pl.rowmin);
     f64s_commit_kernel<<<1, 1024, 0, s>>>(pl.flag, st, rec, cntgw_col_stride(CNTGW_F64S, kd, sq_flag),
                                           kd + (sq_flag ? 1 : 0), mpad, pl.c_plan, pl.key, row_feat, col_rec, n, m,
                                           pl.next_measure);

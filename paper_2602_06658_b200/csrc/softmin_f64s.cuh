@@ -34,7 +34,8 @@ namespace cntgw {
 
 struct F64sArgs {
   const int64_t* row_order;  // ordered position -> caller row (rows block)
-  const int* replan;         // device flag from f64s_check_kernel
+  const int* replan;         // this sweep measures (writes tmin for the stages it walks)
+  const int* full;           // ... and walks every stage (else only the re-vote's kept ones)
   const uint8_t* need;       // [row groups][stages] (row group = one CTA's rows)
   float* tmin;               // [n][stages] min q per row and stage (replan sweeps)
   int stages;                // mpad / TD
@@ -95,11 +96,12 @@ __global__ void select_order_kernel(const double* gamma, int de, const int64_t* 
 
 // (1 block) replan = first sweep / new key; the counter of needed pairs = 0
 __global__ void f64s_begin_kernel(const cntgw_sweep_state* st, CtrPlanKey* key, const void* rows,
-                                  const void* cols, int64_t n, int64_t m, int* flag, int* counter) {
+                                  const void* cols, int64_t n, int64_t m, int* flag, int* counter, int* full) {
   const double lam = st ? st->lam_d : 0.0;
   const bool first = st == nullptr || st->sweep <= 1 || key->lam != lam || key->rows != rows ||
                      key->cols != cols || key->n != n || key->m != m;
   *flag = first ? 1 : 0;
+  *full = first ? 1 : 0;  // a measurement over every stage (else: over the kept ones)
   *counter = 0;
 }
 
@@ -108,7 +110,7 @@ __global__ void f64s_begin_kernel(const cntgw_sweep_state* st, CtrPlanKey* key, 
 // a NaN record or planned constant forces a measurement
 __global__ void __launch_bounds__(128) f64s_shift_kernel(const double* rec, int stride, int off, int64_t m,
                                                          int tile, const double* c_plan, double2* range,
-                                                         int* flag) {
+                                                         int* flag, int* full) {
   __shared__ double smn[4], smx[4];
   const int64_t j0 = (int64_t)blockIdx.x * tile;
   double mn = CUDART_INF, mx = -CUDART_INF;
@@ -123,7 +125,10 @@ __global__ void __launch_bounds__(128) f64s_shift_kernel(const double* rec, int 
     mn = fmin(mn, d);
     mx = fmax(mx, d);
   }
-  if (bad) atomicOr(flag, 1);
+  if (bad) {
+    atomicOr(flag, 1);
+    atomicOr(full, 1);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
@@ -147,18 +152,29 @@ __global__ void __launch_bounds__(128) f64s_shift_kernel(const double* rec, int 
 // row's minimum Mq_i and argmin stage t*_i over the stage minima, and per
 // (group, stage) the smallest relative minimum gmin = min_i (tmin[i][t] -
 // Mq_i) (rounded down). The per-sweep re-vote reads only gmin and t*, not the
-// [n][stages] tmin (16 GB at N = M = 2^20).
-__global__ void __launch_bounds__(256) f64s_reduce_kernel(const int* flag, const float* tmin, int64_t n,
-                                                          int stages, int grows, float* gmin, int* tstar) {
+// [n][stages] tmin (16 GB at N = M = 2^20). A PARTIAL measurement (re-measure
+// within a loop) walked only the stages the re-vote kept; a stage it skipped
+// keeps the re-vote's lower bound of its minimum, Mq_i(old) + gmin(old) +
+// dmin_t (valid in the current frame, and > the row minimum + T), so the new
+// plan stays a plan of lower bounds.
+__global__ void __launch_bounds__(256) f64s_reduce_kernel(const int* flag, const int* full, const float* tmin,
+                                                          const uint8_t* need, const double2* range, int64_t n,
+                                                          int stages, int grows, float* gmin, int* tstar,
+                                                          double* rowmin) {
   if (!*flag) return;
-  extern __shared__ double rmin[];  // [grows]
+  const bool all = *full != 0;
+  extern __shared__ double rsh[];  // [grows] new row minima | [grows] previous ones
+  double* rnew = rsh;
+  double* rold = rsh + grows;
   const int64_t r0 = (int64_t)blockIdx.x * grows;
+  const uint8_t* nd = need + (int64_t)blockIdx.x * stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int r = warp; r < grows; r += nw) {
     float mn = CUDART_INF_F;
     int at = 0;
     if (r0 + r < n)
       for (int t = lane; t < stages; t += 32) {
+        if (!all && !nd[t]) continue;
         const float v = tmin[(r0 + r) * stages + t];
         if (v < mn) {
           mn = v;
@@ -175,24 +191,32 @@ __global__ void __launch_bounds__(256) f64s_reduce_kernel(const int* flag, const
       }
     }
     if (lane == 0) {
-      rmin[r] = mn;
+      rnew[r] = mn;
+      rold[r] = r0 + r < n ? rowmin[r0 + r] : 0.0;
       if (r0 + r < n) tstar[r0 + r] = at;
     }
   }
   __syncthreads();
   // the stage minima were rounded down to fp32: the rows' true minima can sit
-  // up to an ulp of |Mq| above rmin, so gmin is lowered by two ulps of the
+  // up to an ulp of |Mq| above rnew, so gmin is lowered by two ulps of the
   // group's largest |Mq| (keeps every bound of the vote conservative)
   double amax = 0.0;
   for (int r = 0; r < grows && r0 + r < n; ++r)
-    if (fabs(rmin[r]) < CUDART_INF) amax = fmax(amax, fabs(rmin[r]));
+    if (fabs(rnew[r]) < CUDART_INF) amax = fmax(amax, fabs(rnew[r]));
   const double allow = amax * 0x1p-22;
   for (int t = threadIdx.x; t < stages; t += blockDim.x) {
+    const bool walked = all || nd[t];
+    const double gold = walked ? 0.0 : (double)gmin[(int64_t)blockIdx.x * stages + t] + range[t].x;
     double g = CUDART_INF;
-    for (int r = 0; r < grows && r0 + r < n; ++r)
-      g = fmin(g, (double)tmin[(r0 + r) * stages + t] - rmin[r]);  // (inf - inf: an empty row, NaN dropped)
+    for (int r = 0; r < grows && r0 + r < n; ++r) {
+      const double v = walked ? (double)tmin[(r0 + r) * stages + t] : rold[r] + gold;
+      g = fmin(g, v - rnew[r]);  // (inf - inf: an empty row, NaN dropped)
+    }
     gmin[(int64_t)blockIdx.x * stages + t] = __double2float_rd(g - allow);
   }
+  __syncthreads();
+  for (int r = threadIdx.x; r < grows; r += blockDim.x)
+    if (r0 + r < n) rowmin[r0 + r] = rnew[r];
 }
 
 // One block per row group (skipped on a measuring sweep). For a row i of the
@@ -228,16 +252,17 @@ __global__ void __launch_bounds__(256) f64s_vote_kernel(const int* flag, const f
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(counter, cnt);
 }
 
-// (1 thread) measure anew when the re-vote kept too much, and on a geometric
-// schedule (sweeps 8, 16, 32, ... of a loop) while it keeps more than 2%: the
-// plan measured early in a loop reflects transient potentials, and the
-// re-vote only ever loosens it (a measurement costs ~1.2 dense sweeps)
+// (1 thread) measure anew when the re-vote kept too much, and on a schedule
+// (every sweep up to the 8th, then 16, 32, ...) while it keeps more than
+// 0.2%: a plan measured early in a loop reflects transient potentials, and
+// the re-vote only ever loosens it. Within a loop a measurement walks only the
+// kept stages (~1.3 sparse sweeps); the first one of a loop is dense.
 __global__ void f64s_decide_kernel(const cntgw_sweep_state* st, int* flag, const int* counter,
                                    const int* next_measure, int64_t pairs, double max_frac, int schedule) {
   if (*flag) return;
   const double kept = (double)*counter / (double)pairs;
   const int sweep = st ? st->sweep : 0;
-  if (kept > max_frac || (schedule && sweep >= *next_measure && kept > 0.02)) *flag = 1;
+  if (kept > max_frac || (schedule && sweep >= *next_measure && kept > 0.002)) *flag = 1;
 }
 
 // diagnostics: needed (group, stage) pairs of the current mask and the flag
@@ -264,7 +289,9 @@ __global__ void __launch_bounds__(1024) f64s_commit_kernel(const int* flag, cons
   for (int64_t j = threadIdx.x; j < mpad; j += blockDim.x) c_plan[j] = rec[j * stride + off];
   if (threadIdx.x == 0) {
     const int sweep = st ? st->sweep : 0;
-    *next_measure = 2 * sweep > 8 ? 2 * sweep : 8;
+    // partial re-measurements cost ~1.3 sparse sweeps: every sweep while the
+    // early potentials move fast, then at sweeps 16, 32, 64, ...
+    *next_measure = sweep < 8 ? sweep + 1 : 2 * sweep;
     key->lam = st ? st->lam_d : 0.0;
     key->rows = rows;
     key->cols = cols;
@@ -342,7 +369,7 @@ __global__ void __launch_bounds__(128, MINB) softmin_f64s_kernel(const SoftminAr
   const double* rf = reinterpret_cast<const double*>(rb + align256(sizeof(int64_t) * a.n));
   const double* rs = reinterpret_cast<const double*>(rb + align256(sizeof(int64_t) * a.n) +
                                                      align256(sizeof(double) * a.n * KD));
-  const bool replan = *p.replan != 0;
+  const bool replan = *p.replan != 0, full = *p.full != 0;
 
   double afr[RG][KS];
   double mq[RG], S[RG];
@@ -373,7 +400,7 @@ __global__ void __launch_bounds__(128, MINB) softmin_f64s_kernel(const SoftminAr
     const uint8_t* nd = p.need + (int64_t)blockIdx.x * p.stages + t0;
     for (int base = 0; base < ntiles; base += blockDim.x) {
       const int t = base + threadIdx.x;
-      const bool take = t < ntiles && (replan || nd[t]);
+      const bool take = t < ntiles && (full || nd[t]);
       const unsigned ball = __ballot_sync(0xffffffffu, take);
       // warp-ordered append: keep the stages in increasing order
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
