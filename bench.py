@@ -26,8 +26,9 @@ The second half of the BASELINE metric, GW solve time at N=M=2^20, is the
 ``solve`` object of the same line (``--no-solve`` skips it): the C4 config
 (10 outer steps x 100 Sinkhorn sweeps at eps = 0.01, the automatic kernel
 path) through the public solver state from host arrays, CUDA events around
-the whole solve, clocks sampled while it runs; beside it the C1 solve on the
-GPU and the CPU oracle's C1 solve on the host cores.
+the whole solve, clocks sampled while it runs; beside it the C5 (2^18,
+10 x 200) and C3 (1e5, eps-stage chain) solves, the C1 solve on the GPU and
+the CPU oracle's C1 solve on the host cores.
 """
 
 from __future__ import annotations
@@ -64,6 +65,7 @@ def parse():
     p.add_argument("--no-solve", action="store_true", help="skip the GW solve-time block")
     p.add_argument("--solve-n", type=int, default=1 << 20, help="C4 solve size (N=M)")
     p.add_argument("--solve-outer", type=int, default=10)
+    p.add_argument("--no-c5", action="store_true", help="skip the C5 solve in the solve block")
     p.add_argument("--backend", default=None, choices=[None, "nccl", "gloo"],
                    help="collective backend under torchrun (default nccl; gloo only for "
                         "single-GPU functional checks of the multi-rank path)")
@@ -501,38 +503,70 @@ def gw_solve_block(args, info, dev):
     out["c1"] = {"config": "C1 (N=M=1000, eps=0.01, tau=1e-5, <=20 outer)",
                  "seconds": max_ranks(e0.elapsed_time(e1) * 1e-3), "outer": len(res.trace),
                  "inner_iters": list(res.trace.inner_iters), "value": res.value}
-    # C4 at full size
-    n, outer, inner = args.solve_n, args.solve_outer, 100
-    pc = configs.c4(seed=0, n=n)
-    src, tgt = measures(pc)
-    cfg = P.make_config(configs.C4_EPS, n_inner=inner, max_outer=outer)
-    barrier()
-    with ClockSampler(dev.index) as clocks:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        st = solvers._CntGwState(src, tgt, cfg)
-        objs, errs = [], []
-        for _ in range(outer):
-            s = st.step()
-            objs.append(s.objective)
-            errs.append(s.marginal_err)
-        e1.record()
+    paths = {0: "fp32", 1: "fp64 DMMA", 2: "tcgen05 3xTF32", 3: "block-sparse centred fp32 (F32C)",
+             4: "fp64 DMMA + measured block-sparse plan (F64S)"}
+
+    def stepped(key, pc, eps, inner, outer, label):
+        """The config's outer steps through the solver state, timed on the device."""
+        n = pc.x.shape[0]
+        src, tgt = measures(pc)
+        cfg = P.make_config(eps, n_inner=inner, max_outer=outer)
         barrier()
-    secs = max_ranks(e0.elapsed_time(e1) * 1e-3)
-    passes = outer * (2 * inner + 2)  # 2 half-updates per sweep + final tentative + K4 pass
-    out["c4"] = {
-        "config": f"C4 (N=M={n}, d=3, eps=0.01, {outer} outer x {inner} sweeps)",
-        "seconds": secs, "n_gpus": info.world, "objectives": objs, "marginal_errs": errs,
-        "precision_path": {0: "fp32", 1: "fp64 DMMA", 2: "tcgen05 3xTF32",
-                           3: "block-sparse centred fp32 (F32C)",
-                           4: "fp64 DMMA + measured block-sparse plan (F64S)"}.get(int(st.dev.prec),
-                                                                                   str(int(st.dev.prec))),
-        "nm_pairs_per_s": passes * float(n) * n / secs,
-        "timing": "CUDA events around state setup + all outer steps (host arrays in), max over ranks",
-        "clocks": clocks.summary(),
-    }
-    del st
-    torch.cuda.empty_cache()
+        with ClockSampler(dev.index) as clocks:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            st = solvers._CntGwState(src, tgt, cfg)
+            objs, errs = [], []
+            for _ in range(outer):
+                s = st.step()
+                objs.append(s.objective)
+                errs.append(s.marginal_err)
+            e1.record()
+            barrier()
+        secs = max_ranks(e0.elapsed_time(e1) * 1e-3)
+        passes = outer * (2 * inner + 2)  # 2 half-updates per sweep + final tentative + K4 pass
+        out[key] = {
+            "config": label, "seconds": secs, "n_gpus": info.world, "objectives": objs,
+            "marginal_errs": errs, "precision_path": paths.get(int(st.dev.prec), str(int(st.dev.prec))),
+            "nm_pairs_per_s": passes * float(n) * n / secs,
+            "timing": "CUDA events around state setup + all outer steps (host arrays in), max over ranks",
+            "clocks": clocks.summary(),
+        }
+        del st
+        torch.cuda.empty_cache()
+
+    # C4 at full size: the metric's N = M = 2^20 solve
+    n, outer = args.solve_n, args.solve_outer
+    stepped("c4", configs.c4(seed=0, n=n), configs.C4_EPS, 100, outer,
+            f"C4 (N=M={n}, d=3, eps=0.01, {outer} outer x 100 sweeps)")
+    if not args.no_c5:  # C5 at full size (N=M=2^18, D=64 / E=32, 10 x 200)
+        stepped("c5", configs.c5(seed=0), configs.C5_EPS, 200, 10,
+                "C5 (N=M=262144, D=64/E=32, eps=0.02, 10 outer x 200 sweeps)")
+    # C3 at full size: the eps-stage chain (tau = 1e-5) through solve_cnt_gw
+    from dataclasses import replace
+
+    pc = configs.c3(seed=0)
+    src, tgt = measures(pc)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    prev, values, err = None, [], ""
+    for eps in configs.C3_EPS_STAGES:
+        cfg = P.make_config(eps, threshold=1e-5, max_outer=10)
+        warm = None
+        if prev is not None:
+            cfg = replace(cfg, init="gamma", init_gamma=prev.gamma)
+            warm = (prev.coupling.f, prev.coupling.g)
+        try:
+            prev = P.solve_cnt_gw(src, tgt, cfg, _warm_potentials=warm)
+        except P.SolverError as exc:
+            err = f"{eps}: {exc}"
+            break
+        values.append(prev.value)
+    e1.record()
+    barrier()
+    out["c3"] = {"config": "C3 (N=M=100000, 6 eps stages x <=10 outer, tau=1e-5)",
+                 "seconds": max_ranks(e0.elapsed_time(e1) * 1e-3), "stage_values": values, "error": err}
     return out
 
 
