@@ -36,8 +36,12 @@ def timed_steps(src, tgt, cfg, steps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     objs, iters = [], []
+    global STEP_S
+    STEP_S = []
     for _ in range(steps):
-        s = st.step()
+        t1 = time.perf_counter()
+        s = st.step()  # (ends with a host read of the reductions: synchronised)
+        STEP_S.append(round(time.perf_counter() - t1, 3))
         objs.append(s.objective)
         iters.append(s.inner_iters)
     torch.cuda.synchronize()
@@ -70,7 +74,7 @@ def main():
         dt, objs, iters, prec = timed_steps(src, tgt, cfg, outer)
         passes = outer * (2 * inner + 2)
         out = dict(config=which.upper(), n=n, seconds=dt, outer=outer, inner=inner,
-                   objectives=objs, precision_path=int(prec),
+                   objectives=objs, precision_path=int(prec), step_seconds=STEP_S,
                    pairs_per_s=passes * float(n) * n / dt)
     elif which == "c3":
         n = args[0] if args else 100_000
