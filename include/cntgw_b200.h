@@ -200,7 +200,8 @@ size_t cntgw_f64s_rows_bytes(int64_t n, int kd);
 int cntgw_prep_rows_f64s(int kd, int sq_flag, const double* feat, int64_t ld, const double* sq,
                          const int64_t* order, int64_t n, void* rows, void* stream);
 /* Diagnostics of the plan in an F64S workspace: out (3 int64, device) =
- * [needed (row group, stage) pairs, all pairs, 1 if the last sweep measured]. */
+ * [needed (row group, stage) pairs, all pairs, flags of the last sweep: bit 0
+ * measured with the fp64 kernel, bit 1 planned by the fp32 probe]. */
 int cntgw_f64s_plan_density(int kd, int sq_flag, int64_t n, int64_t m, const void* workspace, int64_t* out,
                             void* stream);
 /* out = (Gamma == 0 ? order_if_zero : order_otherwise), decided on the device

@@ -12,6 +12,7 @@
 #include "softmin_ctr_tc.cuh"
 #include "softmin_dmma.cuh"
 #include "softmin_f64s.cuh"
+#include "softmin_f64s_probe.cuh"
 #include "reduce_ctr.cuh"
 #include "softmin_tc.cuh"
 #include "sweep.cuh"
@@ -100,6 +101,10 @@ struct KernelPick {
   int ctr_kx = 0;        // CNTGW_F32C FFMA2 kernel: feature width and groups per CTA
   int ctr_r = 0;         //   (block-sparse plan, ctr_plan_kernel)
   int f64s_tile = 0;     // CNTGW_F64S: column stage of the measured plan (kernel takes F64sArgs)
+  void* probe_fn = nullptr;  // CNTGW_F64S, kd + sq <= 8: the fp32 probe of a dense measurement
+  void* probe_prep_fn = nullptr;
+  int probe_rows = 0;        //   rows per probe CTA (128 threads x R)
+  int probe_p = 0;           //   floats per fp32 probe record
 };
 
 // CNTGW_F64S: the DMMA kernel's tiling (same choices as pick<F64>) on ordered
@@ -115,6 +120,13 @@ KernelPick pick_f64s() {
   k.smem = (size_t)2 * TD * ColLayout<double, KD, SQ>::kStride * sizeof(double);
   k.rec_bytes = ColLayout<double, KD, SQ>::kStride * sizeof(double);
   k.f64s_tile = TD;
+  if constexpr (KD + SQ <= 8) {
+    constexpr int R = KD + SQ <= 4 ? 16 : 8;
+    k.probe_fn = (void*)f64s_probe_kernel<KD, SQ, R, TD>;
+    k.probe_prep_fn = (void*)f64s_probe_prep_kernel<KD + SQ>;
+    k.probe_rows = 128 * R;
+    k.probe_p = ProbeLayout<KD + SQ>::kP;
+  }
   return k;
 }
 
@@ -223,7 +235,7 @@ size_t ctr_plan_bytes(const KernelPick& k, int64_t n, int64_t m) {
 // Measured plan of the CNTGW_F64S kernel: tmin [n][stages] fp32, need
 // [row tiles][stages] bytes, c at the last plan [mpad] fp64, CtrPlanKey.
 struct F64sPlanLayout {
-  size_t tmin, need, cplan, range, gmin, tstar, rowmin, total;
+  size_t tmin, need, cplan, range, gmin, tstar, rowmin, rec32, sbound, total;
   int stages;
   int64_t row_tiles;
 };
@@ -240,7 +252,10 @@ F64sPlanLayout f64s_layout(const KernelPick& k, int64_t n, int64_t m) {
   l.gmin = align256(sizeof(float) * (size_t)l.row_tiles * l.stages);
   l.tstar = align256(sizeof(int) * (size_t)n);
   l.rowmin = align256(sizeof(double) * (size_t)n);
-  l.total = l.tmin + l.need + l.cplan + l.range + l.gmin + l.tstar + l.rowmin + 256;  // + CtrPlanKey, flags
+  l.rec32 = k.probe_fn ? align256(sizeof(float) * (size_t)mpad * k.probe_p) : 0;
+  l.sbound = k.probe_fn ? align256(sizeof(float) * (size_t)l.stages * k.probe_p) : 0;
+  l.total = l.tmin + l.need + l.cplan + l.range + l.gmin + l.tstar + l.rowmin + 256 + l.rec32 + l.sbound;
+  // (the 256 bytes after rowmin: CtrPlanKey, flags)
   return l;
 }
 
@@ -258,6 +273,11 @@ struct F64sPlan {
   int* counter;
   int* next_measure;
   int* full;
+  int* nan;        // the probe stands down (non-finite records)
+  int* probe_ok;   // this sweep's plan came from the probe
+  float* slack;    // the probe's 2 max E (log2 units)
+  float* rec32;    // fp32 probe records [mpad][P]
+  float* sbound;   // per stage magnitude bounds [stages][P]
 };
 F64sPlan f64s_plan(void* base_v, const F64sPlanLayout& l) {
   char* base = static_cast<char*>(base_v);
@@ -274,30 +294,90 @@ F64sPlan f64s_plan(void* base_v, const F64sPlanLayout& l) {
   p.counter = reinterpret_cast<int*>(reinterpret_cast<char*>(p.key) + 128);
   p.next_measure = p.counter + 1;
   p.full = p.counter + 2;
+  p.nan = p.counter + 3;
+  p.probe_ok = p.counter + 4;
+  p.slack = reinterpret_cast<float*>(p.counter + 5);
+  char* tail = base + l.tmin + l.need + l.cplan + l.range + l.gmin + l.tstar + l.rowmin + 256;
+  p.rec32 = l.rec32 ? reinterpret_cast<float*>(tail) : nullptr;
+  p.sbound = l.sbound ? reinterpret_cast<float*>(tail + l.rec32) : nullptr;
   return p;
 }
 
 // Re-vote the measured plan for the current records (f64s_* kernels,
 // softmin_f64s.cuh); leaves *flag = 1 when the sweep must measure anew (or,
 // for a consumer such as K4, walk every stage).
-int f64s_revote(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl, const cntgw_sweep_state* st,
-                const double* rec, int kd, int sq, const void* rows, const void* cols, int64_t n, int64_t m,
-                cudaStream_t s, int schedule) {
+// (gate: run only when *gate, e.g. the re-vote after a probe)
+int f64s_vote(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl, const cntgw_sweep_state* st,
+              const double* rec, int kd, int sq, int64_t n, int64_t m, cudaStream_t s, int schedule,
+              const int* gate, int skip) {
   const int stride = (kd + sq + 1 + 1) / 2 * 2 > (kd + sq + 3) / 4 * 4 ? (kd + sq + 1 + 1) / 2 * 2
                                                                        : (kd + sq + 3) / 4 * 4;
-  f64s_begin_kernel<<<1, 1, 0, s>>>(st, pl.key, rows, cols, n, m, pl.flag, pl.counter, pl.full);
   f64s_shift_kernel<<<(unsigned)l.stages, 128, 0, s>>>(rec, stride, kd + sq, m, k.f64s_tile, pl.c_plan, pl.range,
-                                                        pl.flag, pl.full);
+                                                        pl.flag, pl.full, gate);
   const char* te = getenv("CNTGW_CTR_SKIP_T");
   const double T = te ? atof(te) : 64.0;
   f64s_vote_kernel<<<(unsigned)l.row_tiles, 256, 0, s>>>(pl.flag, pl.gmin, pl.tstar, pl.range, n, l.stages,
-                                                         k.cta_rows, T, pl.need, pl.counter);
+                                                         k.cta_rows, T, pl.need, pl.counter, gate);
   const char* fe = getenv("CNTGW_F64S_REMEASURE");
   const double frac = fe ? atof(fe) : 0.25;
   f64s_decide_kernel<<<1, 1, 0, s>>>(st, pl.flag, pl.counter, pl.next_measure, l.row_tiles * (int64_t)l.stages,
-                                     frac, schedule);
-  return check_launch("f64s_revote");
+                                     frac, schedule, gate, skip);
+  return check_launch("f64s_vote");
 }
+int f64s_revote(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl, const cntgw_sweep_state* st,
+                const double* rec, int kd, int sq, const void* rows, const void* cols, int64_t n, int64_t m,
+                cudaStream_t s, int schedule, int skip) {
+  f64s_begin_kernel<<<1, 1, 0, s>>>(st, skip, pl.key, rows, cols, n, m, pl.flag, pl.counter, pl.full);
+  return f64s_vote(k, l, pl, st, rec, kd, sq, n, m, s, schedule, nullptr, skip);
+}
+
+// The fp32 probe of a dense measurement (softmin_f64s_probe.cuh), all gated on
+// the device flags: prep + row check (iff *full), gate, probe, reduce and
+// commit of its plan, then the re-vote on it. Leaves the sweep non-measuring
+// (or a partial measurement when the probe's plan keeps too much).
+int f64s_probe(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl, const cntgw_sweep_state* st,
+               int skip, const double* rec, int kd, int sq, const void* rows, const void* cols, int64_t n, int64_t m,
+               cudaStream_t s) {
+  const int stride = cntgw_col_stride(CNTGW_F64S, kd, sq);
+  const int64_t mpad = (m + kColTile - 1) / kColTile * kColTile;
+  cudaMemsetAsync(pl.nan, 0, sizeof(int), s);
+  {
+    void* args[] = {(void*)&pl.full, (void*)&rec, (void*)&stride, (void*)&m, (void*)&k.f64s_tile,
+                    (void*)&pl.rec32, (void*)&pl.sbound, (void*)&pl.nan};
+    const cudaError_t e = cudaLaunchKernel(k.probe_prep_fn, dim3(l.stages), dim3(128), args, 0, s);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(CNTGW_ECUDA, "f64s probe prep: %s", cudaGetErrorString(e));
+    }
+  }
+  f64s_probe_rows_check_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1184), 256, 0, s>>>(
+      pl.full, rows, n, kd, sq, pl.nan);
+  f64s_probe_gate_kernel<<<1, 1, 0, s>>>(pl.full, pl.nan, pl.probe_ok, pl.slack);
+  {
+    const int64_t rt = (n + k.probe_rows - 1) / k.probe_rows;
+    // enough CTAs for ~4 waves of 2 per SM: split the stages into chunks
+    int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(l.stages, (148 * 8 + rt - 1) / rt));
+    const int cs = (l.stages + chunks - 1) / chunks;
+    chunks = (l.stages + cs - 1) / cs;
+    const size_t smem = (size_t)2 * k.f64s_tile * k.probe_p * sizeof(float);
+    int stages = l.stages;
+    void* args[] = {(void*)&st, (void*)&skip, (void*)&pl.probe_ok, (void*)&rows, (void*)&n, (void*)&pl.rec32,
+                    (void*)&pl.sbound, (void*)&stages, (void*)&cs, (void*)&pl.tmin, (void*)&pl.slack};
+    const cudaError_t e = cudaLaunchKernel(k.probe_fn, dim3((unsigned)rt, (unsigned)chunks), dim3(128), args, smem, s);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(CNTGW_ECUDA, "f64s probe: %s", cudaGetErrorString(e));
+    }
+  }
+  f64s_reduce_kernel<<<(unsigned)l.row_tiles, 256, 2 * sizeof(double) * k.cta_rows, s>>>(
+      pl.probe_ok, pl.probe_ok, pl.tmin, pl.need, pl.range, n, l.stages, k.cta_rows, pl.gmin, pl.tstar, pl.rowmin,
+      0.f, pl.slack);
+  f64s_commit_kernel<<<1, 1024, 0, s>>>(pl.probe_ok, st, rec, stride, kd + sq, mpad, pl.c_plan, pl.key, rows, cols,
+                                        n, m, pl.next_measure);
+  f64s_probed_kernel<<<1, 1, 0, s>>>(pl.probe_ok, pl.flag, pl.full, pl.counter);
+  return f64s_vote(k, l, pl, st, rec, kd, sq, n, m, s, 1, pl.probe_ok, skip);
+}
+bool f64s_probe_enabled(const KernelPick& k) { return k.probe_fn != nullptr && env_int("CNTGW_F64S_PROBE", 1) != 0; }
 size_t f64s_plan_bytes(const KernelPick& k, int64_t n, int64_t m) { return f64s_layout(k, n, m).total; }
 
 // CNTGW_F32C, kx <= 4, on tcgen05 (softmin_ctr_tc.cuh), opt-in with CNTGW_CTR_TC=1:
@@ -818,10 +898,14 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
     fs.replan = pl.flag;
     fs.stages = fl.stages;
     const double* rec = static_cast<const double*>(col_rec);
-    if (const int rc = f64s_revote(k, fl, pl, st, rec, kd, sq_flag ? 1 : 0, row_feat, col_rec, n, m, s, 1))
+    if (const int rc = f64s_revote(k, fl, pl, st, rec, kd, sq_flag ? 1 : 0, row_feat, col_rec, n, m, s, 1,
+                                   skip_if_done))
       return rc;
-    if (env_int("CNTGW_CTR_REUSE", 1) == 0) f64s_begin_kernel<<<1, 1, 0, s>>>(nullptr, pl.key, row_feat, col_rec,
+    if (env_int("CNTGW_CTR_REUSE", 1) == 0) f64s_begin_kernel<<<1, 1, 0, s>>>(nullptr, 0, pl.key, row_feat, col_rec,
                                                                                 n, m, pl.flag, pl.counter, pl.full);
+    if (f64s_probe_enabled(k))
+      if (const int rc = f64s_probe(k, fl, pl, st, skip_if_done, rec, kd, sq_flag ? 1 : 0, row_feat, col_rec, n, m, s))
+        return rc;
     fs.full = pl.full;
     void* args2[] = {&a, &fs};
     cudaError_t e2 = cudaLaunchKernel(k.fn, dim3(p.row_tiles, p.nchunks), dim3(k.threads), args2, k.smem, s);
@@ -831,7 +915,8 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
     }
     const int64_t mpad = (m + kColTile - 1) / kColTile * kColTile;
     f64s_reduce_kernel<<<(unsigned)fl.row_tiles, 256, 2 * sizeof(double) * k.cta_rows, s>>>(
-        pl.flag, pl.full, pl.tmin, pl.need, pl.range, n, fl.stages, k.cta_rows, pl.gmin, pl.tstar, pl.rowmin);
+        pl.flag, pl.full, pl.tmin, pl.need, pl.range, n, fl.stages, k.cta_rows, pl.gmin, pl.tstar, pl.rowmin,
+        0.f, nullptr);  // (the fp64 kernel measures exact stage minima: no slack)
     f64s_commit_kernel<<<1, 1024, 0, s>>>(pl.flag, st, rec, cntgw_col_stride(CNTGW_F64S, kd, sq_flag),
                                           kd + (sq_flag ? 1 : 0), mpad, pl.c_plan, pl.key, row_feat, col_rec, n, m,
                                           pl.next_measure);
@@ -882,8 +967,9 @@ int cntgw_softmin_dense(const cntgw_sweep_state* st, int skip_if_done, const dou
 }
 
 /* ---- CNTGW_F64S plan diagnostics: out[0] needed (row group, stage) pairs of
- * the mask the last sweep used, out[1] all pairs, out[2] 1 if that sweep
- * measured (walked every stage); out: 3 int64 on the device (out[0] summed) */
+ * the mask the last sweep used, out[1] all pairs, out[2] bit 0: that sweep
+ * measured with the fp64 kernel, bit 1: its plan came from the fp32 probe;
+ * out: 3 int64 on the device (out[0] summed) */
 int cntgw_f64s_plan_density(int kd, int sq_flag, int64_t n, int64_t m, const void* workspace, int64_t* out,
                             void* stream) {
   KernelPick k;
@@ -894,7 +980,8 @@ int cntgw_f64s_plan_density(int kd, int sq_flag, int64_t n, int64_t m, const voi
   const F64sPlan pl = f64s_plan(static_cast<char*>(const_cast<void*>(workspace)) + part_bytes, fl);
   cudaStream_t s = as_stream(stream);
   cudaMemsetAsync(out, 0, sizeof(int64_t), s);
-  f64s_density_kernel<<<148, 256, 0, s>>>(pl.need, fl.row_tiles * (int64_t)fl.stages, pl.flag, out);
+  f64s_density_kernel<<<148, 256, 0, s>>>(pl.need, fl.row_tiles * (int64_t)fl.stages, pl.flag,
+                                          f64s_probe_enabled(k) ? pl.probe_ok : nullptr, out);
   return check_launch("f64s_density");
 }
 
@@ -1045,7 +1132,7 @@ int cntgw_plan_reduce_f64s(const cntgw_sweep_state* st, int kd, int sq_flag, int
   const F64sPlan pl = f64s_plan(static_cast<char*>(plan_ws) + part_bytes, fl);
   const int64_t mpad = cntgw_cols_padded(m);
   // re-vote for the final pair's records; a stale plan (*flag) walks every stage
-  if (const int rc = f64s_revote(k, fl, pl, st, col_rec, kd, 1, f64s_rows, col_rec, n, m, s, 0)) return rc;
+  if (const int rc = f64s_revote(k, fl, pl, st, col_rec, kd, 1, f64s_rows, col_rec, n, m, s, 0, 0)) return rc;
   const uint8_t* need = pl.need;
   const int* stale = pl.flag;
   const int stride_acc = (ep + 1 + 1) / 2 * 2;

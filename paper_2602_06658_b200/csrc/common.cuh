@@ -149,6 +149,12 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) {
   return d;
 }
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+// three-input minimum (FMNMX3)
+__device__ __forceinline__ float fmin3f(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
 
 // ---- mbarrier + 1-D bulk copy (TMA engine, UBLKCP) ------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

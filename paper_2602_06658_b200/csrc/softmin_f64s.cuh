@@ -13,7 +13,9 @@
 // stage) mask derived from MEASURED stage minima, not from geometric bounds:
 //   * a measuring sweep (the first of a loop, see below) walks every stage —
 //     its outputs are exact — and also writes each row's minimum q over each
-//     stage (tmin, fp32 rounded down);
+//     stage (tmin, fp32 rounded down). The dense measurement of a loop's
+//     first sweep is the fp32 probe instead (softmin_f64s_probe.cuh) when the
+//     width allows, and this kernel then walks only the probe's kept stages;
 //   * every later sweep re-votes the mask from tmin and the per-stage range
 //     of the column-constant shifts since the measurement (f64s_shift /
 //     f64s_vote kernels, below) and walks only the needed stages (their
@@ -95,8 +97,14 @@ __global__ void select_order_kernel(const double* gamma, int de, const int64_t* 
 // keeps more than CNTGW_F64S_REMEASURE of the (group, stage) pairs.
 
 // (1 block) replan = first sweep / new key; the counter of needed pairs = 0
-__global__ void f64s_begin_kernel(const cntgw_sweep_state* st, CtrPlanKey* key, const void* rows,
+__global__ void f64s_begin_kernel(const cntgw_sweep_state* st, int skip, CtrPlanKey* key, const void* rows,
                                   const void* cols, int64_t n, int64_t m, int* flag, int* counter, int* full) {
+  if (skip_now(st, skip)) {  // (the loop is done: no sweep, no measurement)
+    *flag = 0;
+    *full = 0;
+    *counter = 0;
+    return;
+  }
   const double lam = st ? st->lam_d : 0.0;
   const bool first = st == nullptr || st->sweep <= 1 || key->lam != lam || key->rows != rows ||
                      key->cols != cols || key->n != n || key->m != m;
@@ -110,8 +118,9 @@ __global__ void f64s_begin_kernel(const cntgw_sweep_state* st, CtrPlanKey* key, 
 // a NaN record or planned constant forces a measurement
 __global__ void __launch_bounds__(128) f64s_shift_kernel(const double* rec, int stride, int off, int64_t m,
                                                          int tile, const double* c_plan, double2* range,
-                                                         int* flag, int* full) {
+                                                         int* flag, int* full, const int* gate) {
   __shared__ double smn[4], smx[4];
+  if (gate && !*gate) return;
   const int64_t j0 = (int64_t)blockIdx.x * tile;
   double mn = CUDART_INF, mx = -CUDART_INF;
   bool bad = false;
@@ -160,7 +169,7 @@ __global__ void __launch_bounds__(128) f64s_shift_kernel(const double* rec, int 
 __global__ void __launch_bounds__(256) f64s_reduce_kernel(const int* flag, const int* full, const float* tmin,
                                                           const uint8_t* need, const double2* range, int64_t n,
                                                           int stages, int grows, float* gmin, int* tstar,
-                                                          double* rowmin) {
+                                                          double* rowmin, float slack_c, const float* slack_p) {
   if (!*flag) return;
   const bool all = *full != 0;
   extern __shared__ double rsh[];  // [grows] new row minima | [grows] previous ones
@@ -203,7 +212,7 @@ __global__ void __launch_bounds__(256) f64s_reduce_kernel(const int* flag, const
   double amax = 0.0;
   for (int r = 0; r < grows && r0 + r < n; ++r)
     if (fabs(rnew[r]) < CUDART_INF) amax = fmax(amax, fabs(rnew[r]));
-  const double allow = amax * 0x1p-22;
+  const double allow = amax * 0x1p-22 + (slack_p ? (double)*slack_p : (double)slack_c);
   for (int t = threadIdx.x; t < stages; t += blockDim.x) {
     const bool walked = all || nd[t];
     const double gold = walked ? 0.0 : (double)gmin[(int64_t)blockIdx.x * stages + t] + range[t].x;
@@ -227,8 +236,8 @@ __global__ void __launch_bounds__(256) f64s_reduce_kernel(const int* flag, const
 // group's rows of dmax_{t*_i}. Counts the needed pairs.
 __global__ void __launch_bounds__(256) f64s_vote_kernel(const int* flag, const float* gmin, const int* tstar,
                                                         const double2* range, int64_t n, int stages, int grows,
-                                                        double T, uint8_t* need, int* counter) {
-  if (*flag) return;
+                                                        double T, uint8_t* need, int* counter, const int* gate) {
+  if (*flag || (gate && !*gate)) return;
   __shared__ double dg_s[8];
   const int64_t r0 = (int64_t)blockIdx.x * grows;
   double dg = -CUDART_INF;
@@ -258,15 +267,17 @@ __global__ void __launch_bounds__(256) f64s_vote_kernel(const int* flag, const f
 // the re-vote only ever loosens it. Within a loop a measurement walks only the
 // kept stages (~1.3 sparse sweeps); the first one of a loop is dense.
 __global__ void f64s_decide_kernel(const cntgw_sweep_state* st, int* flag, const int* counter,
-                                   const int* next_measure, int64_t pairs, double max_frac, int schedule) {
-  if (*flag) return;
+                                   const int* next_measure, int64_t pairs, double max_frac, int schedule,
+                                   const int* gate, int skip) {
+  if (*flag || (gate && !*gate) || skip_now(st, skip)) return;
   const double kept = (double)*counter / (double)pairs;
   const int sweep = st ? st->sweep : 0;
   if (kept > max_frac || (schedule && sweep >= *next_measure && kept > 0.002)) *flag = 1;
 }
 
 // diagnostics: needed (group, stage) pairs of the current mask and the flag
-__global__ void f64s_density_kernel(const uint8_t* need, int64_t pairs, const int* flag, int64_t* out) {
+__global__ void f64s_density_kernel(const uint8_t* need, int64_t pairs, const int* flag, const int* probed,
+                                    int64_t* out) {
   int64_t c = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += (int64_t)gridDim.x * blockDim.x)
     c += need[i] ? 1 : 0;
@@ -275,7 +286,7 @@ __global__ void f64s_density_kernel(const uint8_t* need, int64_t pairs, const in
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)c);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     out[1] = pairs;
-    out[2] = *flag;
+    out[2] = *flag + (probed ? 2 * *probed : 0);
   }
 }
 

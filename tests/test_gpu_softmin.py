@@ -367,3 +367,37 @@ def test_f64s_measured_plan_matches_dense_loop(env, k, anneal, monkeypatch):
     want = O.softmin(O.SqEuclid(x, z), np.log(b), out["f64s"][1], res.coupling.eps_eff, row_idx=rows)
     got = _half_update(env, cost, a, b, out["f64s"][1], res.coupling.eps_eff, 4)
     assert _rel(got[rows], want) < 5e-7
+
+
+@pytest.mark.parametrize("anneal", [None, 0.05], ids=["fixed", "annealed"])
+@pytest.mark.parametrize("k", [3, 4])
+def test_f64s_probe_matches_fp64_measurement(env, k, anneal, monkeypatch):
+    """CNTGW_F64S with the fp32 probe (softmin_f64s_probe.cuh: the dense
+    measurement of each loop's first sweep as fp32 stage minima minus a
+    rigorous error bound) against the fp64 measuring sweep
+    (CNTGW_F64S_PROBE=0): both plans skip only terms below 2^-64 of their
+    rows' maxima, so the loops agree to fp64 rounding; and both equal the
+    dense fp64 loop."""
+    P, engine, S, O, torch, dev = env
+    rng = np.random.default_rng(41 + k)
+    n, m = 1 << 14, 3 << 12
+    cx = rng.standard_normal((16, k)) * 2.0
+    x = cx[rng.integers(0, 16, n)] + rng.standard_normal((n, k)) * 0.5
+    z = cx[rng.integers(0, 16, m)] @ np.linalg.qr(rng.standard_normal((k, k)))[0] \
+        + rng.standard_normal((m, k)) * 0.5
+    a, b = np.full(n, 1 / n), np.full(m, 1 / m)
+    cost = P.SquaredEuclideanCost(x, z)
+    cfg = P.SinkhornConfig(eps=2.5e-3, n_inner=30, anneal_from=anneal)
+    out = {}
+    for tag, prec, probe in (("probe", "f64s", "1"), ("fp64", "f64s", "0"), ("dense", "f64", "1")):
+        monkeypatch.setenv("CNTGW_PRECISION", prec)
+        monkeypatch.setenv("CNTGW_F64S_PROBE", probe)
+        res = P.sinkhorn(a, b, cost, cfg)
+        out[tag] = (res.coupling.f, res.coupling.g)
+    # (the walks differ in which stages they visit, so the lazy reference of
+    # each row rebases at other points and the fp32 exponent arguments round
+    # differently: ~1e-9 relative; the skipped mass itself is < 2^-64)
+    assert _rel(out["probe"][0], out["fp64"][0]) < 5e-9
+    assert _rel(out["probe"][1], out["fp64"][1]) < 5e-9
+    assert _rel(out["probe"][0], out["dense"][0]) < 5e-8
+    assert _rel(out["probe"][1], out["dense"][1]) < 5e-8
