@@ -173,29 +173,40 @@ KernelPick pick() {
   X(PREC, 32, 0) X(PREC, 32, 1) X(PREC, 64, 0) X(PREC, 64, 1)
 
 // Tensor-core variant knobs (read per call so tools can sweep them):
-// CNTGW_TC_POLY in {0,2,4,6} (default 2, fastest in tools/sweep_paths.py):
-// pairs (of 16 per 32-column chunk) whose exp2 runs on the FMA pipe instead of
-// MUFU; CNTGW_TC_EPI in {8,16}: epilogue warps (default 16).
-template <int KD, int EPI>
+// CNTGW_TC_KIND = f16 (default: the 3-way split on fp16 operands, kind::f16)
+// or tf32 (kind::tf32); CNTGW_TC_POLY in {0,2,3,4,6} (default 2, fastest in
+// tools/sweep_paths.py): pairs (of 16 per 32-column chunk) whose exp2 runs on
+// the FMA pipe instead of MUFU; CNTGW_TC_EPI in {8,16}: epilogue warps
+// (default 16).
+bool tc_f16() {
+  const char* e = getenv("CNTGW_TC_KIND");
+  return !(e && (e[0] == 't' || e[0] == 'T'));
+}
+
+template <int KD, int EPI, bool H>
 void* tc_fn(int poly) {
   switch (poly) {
-    case 2: return (void*)softmin_tc_kernel<KD, 2, EPI>;
-    case 4: return (void*)softmin_tc_kernel<KD, 4, EPI>;
-    case 6: return (void*)softmin_tc_kernel<KD, 6, EPI>;
-    default: return (void*)softmin_tc_kernel<KD, 0, EPI>;
+    case 2: return (void*)softmin_tc_kernel<KD, 2, EPI, H>;
+    case 3: return (void*)softmin_tc_kernel<KD, 3, EPI, H>;
+    case 4: return (void*)softmin_tc_kernel<KD, 4, EPI, H>;
+    case 6: return (void*)softmin_tc_kernel<KD, 6, EPI, H>;
+    default: return (void*)softmin_tc_kernel<KD, 0, EPI, H>;
   }
 }
 
 template <int KD>
 KernelPick pick_tc() {
-  using L = TcLayout<KD>;
   KernelPick k;
   const int poly = env_int("CNTGW_TC_POLY", 2);
   const int epi = env_int("CNTGW_TC_EPI", 16) == 8 ? 8 : 16;
-  k.fn = epi == 16 ? tc_fn<KD, 16>(poly) : tc_fn<KD, 8>(poly);
+  const bool h = tc_f16();
+  if (h) k.fn = epi == 16 ? tc_fn<KD, 16, true>(poly) : tc_fn<KD, 8, true>(poly);
+  else k.fn = epi == 16 ? tc_fn<KD, 16, false>(poly) : tc_fn<KD, 8, false>(poly);
   k.rows = 1;  // 128 rows per CTA = 128 threads x 1 in the planner's units
-  k.smem = (size_t)(L::kATileFloats + kTcStages * L::kBTileFloats) * sizeof(float);
-  k.rec_bytes = L::kKp * sizeof(float);
+  const size_t a_bytes = h ? TcLayoutH<KD>::kATileBytes : TcLayout<KD>::kATileBytes;
+  const size_t b_bytes = h ? TcLayoutH<KD>::kBTileBytes : TcLayout<KD>::kBTileBytes;
+  k.smem = a_bytes + kTcStages * b_bytes;
+  k.rec_bytes = h ? TcLayoutH<KD>::kRecBytes : TcLayout<KD>::kRecBytes;
   k.threads = tc_threads(epi);
   return k;
 }
@@ -753,12 +764,24 @@ int cntgw_prep_cols(const cntgw_sweep_state* st, int prec, int kd, int sq_flag, 
   const unsigned blocks = (unsigned)((mpad + th - 1) / th);
   const int sqf = sq_flag ? 1 : 0;
   if (prec == CNTGW_TF32X3) {
-    if (kd == 8)
-      prep_cols_tc_kernel<8><<<blocks, th, 0, as_stream(stream)>>>(
-          st, static_cast<const float*>(feat), ld, pot, log2w, m, mpad, static_cast<float*>(rec));
+    const float* f = static_cast<const float*>(feat);
+    cudaStream_t s = as_stream(stream);
+    if (tc_f16()) {  // absmax of the features (the word after the records), then the fp16 pack
+      const size_t rec_bytes = (size_t)mpad * (kd == 8 ? TcLayoutH<8>::kRecBytes : TcLayoutH<16>::kRecBytes);
+      uint32_t* absmax = reinterpret_cast<uint32_t*>(static_cast<char*>(rec) + rec_bytes);
+      cudaMemsetAsync(absmax, 0, sizeof(uint32_t), s);
+      tc_absmax_kernel<<<(unsigned)std::min<int64_t>((m * kd + 1023) / 1024, 4 * num_sms()), 256, 0, s>>>(
+          f, ld, kd, m, absmax);
+      if (kd == 8)
+        prep_cols_tch_kernel<8><<<blocks, th, 0, s>>>(st, f, ld, pot, log2w, m, mpad, static_cast<__half*>(rec),
+                                                      absmax);
+      else
+        prep_cols_tch_kernel<16><<<blocks, th, 0, s>>>(st, f, ld, pot, log2w, m, mpad, static_cast<__half*>(rec),
+                                                       absmax);
+    } else if (kd == 8)
+      prep_cols_tc_kernel<8><<<blocks, th, 0, s>>>(st, f, ld, pot, log2w, m, mpad, static_cast<float*>(rec));
     else
-      prep_cols_tc_kernel<16><<<blocks, th, 0, as_stream(stream)>>>(
-          st, static_cast<const float*>(feat), ld, pot, log2w, m, mpad, static_cast<float*>(rec));
+      prep_cols_tc_kernel<16><<<blocks, th, 0, s>>>(st, f, ld, pot, log2w, m, mpad, static_cast<float*>(rec));
     return check_launch("prep_cols_tc");
   }
   if (prec == CNTGW_F32)

@@ -28,6 +28,10 @@
 // 16-byte K chunks of one K=8 MMA step.
 #pragma once
 
+#include <cuda_fp16.h>
+
+#include <type_traits>
+
 #include "common.cuh"
 #include "softmin.cuh"
 
@@ -47,7 +51,48 @@ struct TcLayout {
   static constexpr int kATileFloats = kChunks * kTcRows * 4;
   // K' positions of the three blocks
   static constexpr int kHi = 0, kLo = KD + 1, kHi2 = 2 * KD + 2;
+  static constexpr int kATileBytes = kATileFloats * 4, kBTileBytes = kBTileFloats * 4;
+  static constexpr int kMmas = kKp / 8;                  // K = 8 per tf32 instruction
+  static constexpr int kRecBytes = kKp * 4;              // per column
 };
+
+// The same split on fp16 operands (kind::f16, K = 16 per instruction at twice
+// the tf32 rate and half the operand bytes). The tf32 parts hi = tf32(x) and
+// lo = tf32(x - hi) carry 11 significant bits, exactly what fp16 holds, so
+// once both sides are scaled into fp16's exponent range the products are the
+// ones the tf32 MMA forms. Scaling: with 2^eb > max_jk |zt_jk| (an absmax
+// pass over the column features, tc_absmax_kernel) the column side is stored
+// as zt * 2^(14 - eb) (|.| < 2^14) and the row side as x * 2^(eb + 1)
+// (|.| < 4 max|x| max|zt| < 2^14 on this path, whose exponent scale is < 4096);
+// the accumulator then holds t * 2^15 and the epilogue's reference
+// subtraction becomes one FFMA2, x = v * 2^-15 - mref. A value too small for
+// fp16's normal range is off by at most 2^-25 before the 2^14 * 2^-15 of its
+// partner and the rescale, i.e. 2^-26 per product in t. The bias is split in
+// three fp16 parts against 2^15 on the row side.
+//     A'_i = [hi(x_i) | lo(x_i) | hi(x_i)] * 2^(eb+1) | 2^15 2^15 2^15
+//     B'_j = [hi(zt_j) | hi(zt_j) | lo(zt_j)] * 2^(14-eb) | b_hi b_mid b_lo
+template <int KD>
+struct TcLayoutH {
+  static constexpr int kKp = (3 * KD + 3 + 15) / 16 * 16;  // halfs, padded to the MMA K step
+  static constexpr int kChunks = kKp / 8;                   // 16-byte K chunks
+  static constexpr int kATileBytes = kChunks * kTcRows * 16, kBTileBytes = kChunks * kTcCols * 16;
+  static constexpr int kMmas = kKp / 16;
+  static constexpr int kRecBytes = kKp * 2;
+  static constexpr int kHH = 0, kLH = KD, kHL = 2 * KD, kBias = 3 * KD;
+};
+constexpr float kTcHScale = 0x1p-15f;  // accumulator -> log2 units
+constexpr float kTcHPadBias = -60000.f;
+
+// 2^eb > max |2 lam z| from the absmax word (float bits of max |z|)
+__device__ __forceinline__ int tch_col_exp(uint32_t maxbits, float two_lam) {
+  const float mz = fabsf(two_lam) * __uint_as_float(maxbits);
+  if (!(mz > 0.f) || !(mz < CUDART_INF_F)) return 0;
+  return ilogbf(mz) + 1;
+}
+__device__ __forceinline__ float pow2i(int k) {
+  k = k < -126 ? -126 : (k > 127 ? 127 : k);
+  return __int_as_float((127 + k) << 23);
+}
 
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
@@ -78,6 +123,14 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(kTcIdesc), "r"(acc));
+}
+// kind::f16 (fp16 A/B = format 0), fp32 accumulate, K-major, M=128, N=256
+constexpr uint32_t kTcIdescH = (1u << 4) | ((uint32_t)(kTcCols >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
+__device__ __forceinline__ void tc_mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kTcIdescH), "r"(acc));
 }
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -140,25 +193,85 @@ __global__ void prep_cols_tc_kernel(const cntgw_sweep_state* st, const float* fe
   }
 }
 
+// fp16 operands: absmax of the column features (float bits, >= 0, so the
+// unsigned order is the float order), then the pack. The absmax word sits
+// right after the records (byte mpad * kRecBytes), outside the MMA's reads.
+__global__ void tc_absmax_kernel(const float* feat, int64_t ld, int kd, int64_t m, uint32_t* out) {
+  float mx = 0.f;
+  const int64_t total = m * kd;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    mx = fmaxf(mx, fabsf(feat[(idx / kd) * ld + idx % kd]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(out, __float_as_uint(mx));
+}
+
+template <int KD>
+__global__ void prep_cols_tch_kernel(const cntgw_sweep_state* st, const float* feat, int64_t ld,
+                                     const double* pot, const double* log2w, int64_t m, int64_t mpad,
+                                     __half* rec, const uint32_t* absmax) {
+  using L = TcLayoutH<KD>;
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= mpad) return;
+  const int64_t tile = j / kTcCols;
+  const int col = (int)(j % kTcCols);
+  __half* base = rec + tile * (L::kBTileBytes / 2) + col * 8;
+  auto put = [&](int p, float v) { base[(p >> 3) * (kTcCols * 8) + (p & 7)] = __float2half_rn(v); };
+  for (int p = 0; p < L::kKp; ++p) put(p, 0.f);
+  if (j < m) {
+    const double lam = (double)st->lam;
+    const float two_lam = (float)(2.0 * lam);
+    const float sb = pow2i(14 - tch_col_exp(*absmax, two_lam));
+    for (int k = 0; k < KD; ++k) {
+      const float z = two_lam * feat[j * ld + k];
+      const float zh = tf32_rna(z);
+      const float zl = tf32_rna(z - zh);
+      put(L::kHH + k, zh * sb);
+      put(L::kLH + k, zh * sb);
+      put(L::kHL + k, zl * sb);
+    }
+    // (zero-weight columns: log2 w = -inf, kept finite so the parts stay exact)
+    float beta = (float)(lam * (pot ? pot[j] : 0.0) + log2w[j]);
+    if (beta < kTcHPadBias) beta = kTcHPadBias;  // (a NaN stays a NaN)
+    const float b1 = __half2float(__float2half_rn(beta));
+    const float b2 = __half2float(__float2half_rn(beta - b1));
+    put(L::kBias, b1);
+    put(L::kBias + 1, b2);
+    put(L::kBias + 2, beta - b1 - b2);
+  } else {
+    put(L::kBias, kTcHPadBias);  // padding column: 2^(t - max) == 0
+  }
+}
+
 // One 32-column chunk of the epilogue: terms 2^(v - mref) summed with FADD2
 // pairs into four independent accumulators, NPOLY of the 16 pairs exponentiated
 // on the FMA pipe and the rest on MUFU.EX2; a chunk whose sum leaves [0, 2^20]
 // (or is inf/NaN) rebases the row reference at the chunk maximum.
-template <int NPOLY>
+template <int NPOLY, bool SCALED = false>
 __device__ __forceinline__ void tc_chunk(const float (&v)[32], float& mref, float& tsum, FFSum& S) {
+  // SCALED: the accumulator holds t * 2^15 (fp16 operands); the rescale rides
+  // on the reference subtraction as one FFMA2
+  const float2 sc2 = f2(kTcHScale, kTcHScale);
+  auto arg = [&](int u, float2 nm) {
+    const float2 t = f2(v[2 * u], v[2 * u + 1]);
+    return SCALED ? fma2(t, sc2, nm) : add2(t, nm);
+  };
   float2 nm = f2(-mref, -mref);
-  float2 acc[4] = {f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f)};
+  float2 acc[4];
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
-    const float2 x = add2(f2(v[2 * u], v[2 * u + 1]), nm);
+    const float2 x = arg(u, nm);
     // offloaded pairs spread over the four accumulators
     constexpr uint32_t kMask = NPOLY == 2   ? 0x0201u
+                               : NPOLY == 3 ? 0x0421u
                                : NPOLY == 4 ? 0x8421u
                                : NPOLY == 6 ? 0x9249u
                                : NPOLY == 8 ? 0x5555u
                                             : 0u;
     const bool poly = (kMask >> u) & 1u;
-    acc[u & 3] = add2(acc[u & 3], poly ? exp2_poly2(x) : f2(ex2(x.x), ex2(x.y)));
+    const float2 e = poly ? exp2_poly2(x) : f2(ex2(x.x), ex2(x.y));
+    acc[u & 3] = u < 4 ? e : add2(acc[u & 3], e);
   }
   float2 t2 = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
   float csum = t2.x + t2.y;
@@ -166,6 +279,7 @@ __device__ __forceinline__ void tc_chunk(const float (&v)[32], float& mref, floa
     float cm = v[0];
 #pragma unroll
     for (int u = 1; u < 32; ++u) cm = fmaxf(cm, v[u]);
+    if (SCALED) cm *= kTcHScale;
     if (cm > mref) {
       const float sc = ex2(mref - cm);
       S.scale(sc);
@@ -176,7 +290,7 @@ __device__ __forceinline__ void tc_chunk(const float (&v)[32], float& mref, floa
     float2 r = f2(0.f, 0.f);
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      const float2 x = add2(f2(v[2 * u], v[2 * u + 1]), nm);
+      const float2 x = arg(u, nm);
       r = add2(r, f2(ex2(x.x), ex2(x.y)));
     }
     csum = r.x + r.y;
@@ -184,10 +298,10 @@ __device__ __forceinline__ void tc_chunk(const float (&v)[32], float& mref, floa
   tsum += csum;
 }
 
-template <int KD, int NPOLY, int EPI>
+template <int KD, int NPOLY, int EPI, bool H = false>
 __global__ void __launch_bounds__(tc_threads(EPI), 1) softmin_tc_kernel(const SoftminArgs a) {
-  using L = TcLayout<KD>;
-  extern __shared__ __align__(1024) float smem_tc[];
+  using L = std::conditional_t<H, TcLayoutH<KD>, TcLayout<KD>>;
+  extern __shared__ __align__(1024) char smem_tc[];
   __shared__ uint64_t full_bar[kTcStages], empty_bar[kTcStages], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
   constexpr int kParts = EPI / 4;                  // column parts per TMEM quadrant
@@ -196,8 +310,8 @@ __global__ void __launch_bounds__(tc_threads(EPI), 1) softmin_tc_kernel(const So
   __shared__ double red_s[kParts][kTcRows];
   if (skip_now(a.st, a.skip)) return;
 
-  float* sA = smem_tc;                       // A' : kChunks x 128 rows x 16 B
-  float* sB = smem_tc + L::kATileFloats;     // B' : kTcStages stages
+  char* sA = smem_tc;                      // A' : kChunks x 128 rows x 16 B
+  char* sB = smem_tc + L::kATileBytes;     // B' : kTcStages stages
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int chunk = blockIdx.y;
   const int64_t row0 = (int64_t)blockIdx.x * kTcRows;
@@ -227,18 +341,38 @@ __global__ void __launch_bounds__(tc_threads(EPI), 1) softmin_tc_kernel(const So
     const int r = t & (kTcRows - 1), h = t >> 7;
     const int64_t i = row0 + r;
     const float* xf = static_cast<const float*>(a.row_feat);
-    auto put = [&](int p, float v) { sA[(p >> 2) * (kTcRows * 4) + r * 4 + (p & 3)] = v; };
-    for (int k = h * (KD / kParts); k < (h + 1) * (KD / kParts); ++k) {
-      const float x = i < a.n ? xf[i * a.ld_row + k] : 0.f;
-      const float xh = tf32_rna(x);
-      put(L::kHi + k, xh);
-      put(L::kLo + k, xh);
-      put(L::kHi2 + k, tf32_rna(x - xh));
-    }
-    if (h == 0) {
-      put(L::kHi + KD, 1.f);
-      put(L::kLo + KD, 1.f);
-      for (int p = L::kHi2 + KD; p < L::kKp; ++p) put(p, 0.f);
+    if constexpr (H) {
+      __half* hA = reinterpret_cast<__half*>(sA);
+      auto put = [&](int p, float v) { hA[(p >> 3) * (kTcRows * 8) + r * 8 + (p & 7)] = __float2half_rn(v); };
+      const uint32_t absmax = *reinterpret_cast<const uint32_t*>(static_cast<const char*>(a.col_rec) +
+                                                                 mpad * L::kRecBytes);
+      const float sa = pow2i(tch_col_exp(absmax, (float)(2.0 * (double)a.st->lam)) + 1);
+      for (int k = h * (KD / kParts); k < (h + 1) * (KD / kParts); ++k) {
+        const float x = i < a.n ? xf[i * a.ld_row + k] : 0.f;
+        const float xh = tf32_rna(x);
+        put(L::kHH + k, xh * sa);
+        put(L::kLH + k, tf32_rna(x - xh) * sa);
+        put(L::kHL + k, xh * sa);
+      }
+      if (h == 0) {
+        for (int p = 0; p < 3; ++p) put(L::kBias + p, 32768.f);
+        for (int p = L::kBias + 3; p < L::kKp; ++p) put(p, 0.f);
+      }
+    } else {
+      float* fA = reinterpret_cast<float*>(sA);
+      auto put = [&](int p, float v) { fA[(p >> 2) * (kTcRows * 4) + r * 4 + (p & 3)] = v; };
+      for (int k = h * (KD / kParts); k < (h + 1) * (KD / kParts); ++k) {
+        const float x = i < a.n ? xf[i * a.ld_row + k] : 0.f;
+        const float xh = tf32_rna(x);
+        put(L::kHi + k, xh);
+        put(L::kLo + k, xh);
+        put(L::kHi2 + k, tf32_rna(x - xh));
+      }
+      if (h == 0) {
+        put(L::kHi + KD, 1.f);
+        put(L::kLo + KD, 1.f);
+        for (int p = L::kHi2 + KD; p < L::kKp; ++p) put(p, 0.f);
+      }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> tensor-core proxy
   }
@@ -249,12 +383,12 @@ __global__ void __launch_bounds__(tc_threads(EPI), 1) softmin_tc_kernel(const So
 
   if (warp == 0) {
     if (lane == 0) {  // producer
-      const uint32_t bytes = L::kBTileFloats * sizeof(float);
-      const float* src = static_cast<const float*>(a.col_rec) + (c0 / kTcCols) * L::kBTileFloats;
+      const uint32_t bytes = L::kBTileBytes;
+      const char* src = static_cast<const char*>(a.col_rec) + (c0 / kTcCols) * L::kBTileBytes;
       for (int t = 0, s = 0, ph = 0; t < ntiles; ++t) {
         mbar_wait(&empty_bar[s], ph ^ 1);
         mbar_expect_tx(&full_bar[s], bytes);
-        bulk_g2s(sB + s * L::kBTileFloats, src + (int64_t)t * L::kBTileFloats, bytes, &full_bar[s]);
+        bulk_g2s(sB + s * L::kBTileBytes, src + (int64_t)t * L::kBTileBytes, bytes, &full_bar[s]);
         if (++s == kTcStages) s = 0, ph ^= 1;
       }
     }
@@ -266,13 +400,14 @@ __global__ void __launch_bounds__(tc_threads(EPI), 1) softmin_tc_kernel(const So
         mbar_wait(&full_bar[s], ph);
         mbar_wait(&tempty_bar[ab], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t b0 = smem_u32(sB + s * L::kBTileFloats);
+        const uint32_t b0 = smem_u32(sB + s * L::kBTileBytes);
         const uint32_t d = tmem + (uint32_t)(ab * kTcCols);
 #pragma unroll
-        for (int ks = 0; ks < L::kKp / 8; ++ks) {
+        for (int ks = 0; ks < L::kMmas; ++ks) {  // two 16-byte K chunks per instruction
           const uint64_t ad = umma_desc(a0 + ks * 2 * (kTcRows * 16), kTcRows * 16, 128);
           const uint64_t bd = umma_desc(b0 + ks * 2 * (kTcCols * 16), kTcCols * 16, 128);
-          tc_mma(d, ad, bd, ks > 0 ? 1u : 0u);
+          if constexpr (H) tc_mma_f16(d, ad, bd, ks > 0 ? 1u : 0u);
+          else tc_mma(d, ad, bd, ks > 0 ? 1u : 0u);
         }
         tc_commit(&empty_bar[s]);   // smem stage reusable once these MMAs completed
         tc_commit(&tfull_bar[ab]);  // accumulator ab ready for the epilogue
@@ -305,7 +440,7 @@ __global__ void __launch_bounds__(tc_threads(EPI), 1) softmin_tc_kernel(const So
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty_bar[s]);  // accumulator s may be overwritten
         }
-        tc_chunk<NPOLY>(cur, mref, tsum, S);
+        tc_chunk<NPOLY, H>(cur, mref, tsum, S);
         if (c + 1 < kChunksPerPart) tmem_wait_ld();
       }
       S.add(tsum);

@@ -55,12 +55,16 @@ def main(n=1 << 19, reps=3, rounds=3, only=None):
     dev = torch.device("cuda", 0)
     variants = []
     src, tgt, eps, pot = build(n, 16, False)
-    for prec, poly, epi, l2 in [(F32, 0, 8, 32), (TF32X3, 0, 16, 0), (TF32X3, 0, 16, 32),
-                                (TF32X3, 2, 8, 32), (TF32X3, 2, 16, 32), (TF32X3, 4, 16, 32),
-                                (TF32X3, 6, 16, 32)]:
-        variants.append((f"C2 K=16 prec={prec} poly={poly} epi={epi} l2={l2}", src, tgt, eps, pot, prec,
-                         {"CNTGW_TC_POLY": str(poly), "CNTGW_TC_EPI": str(epi),
-                          "CNTGW_L2_CHUNK_MB": str(l2)}))
+    for prec, kind, poly, epi, l2 in [(F32, "-", 0, 8, 32), (TF32X3, "tf32", 0, 16, 32),
+                                      (TF32X3, "tf32", 2, 16, 32), (TF32X3, "tf32", 2, 16, 0),
+                                      (TF32X3, "tf32", 4, 16, 32), (TF32X3, "f16", 0, 16, 32),
+                                      (TF32X3, "f16", 2, 8, 32), (TF32X3, "f16", 2, 16, 32),
+                                      (TF32X3, "f16", 2, 16, 0), (TF32X3, "f16", 2, 16, 64),
+                                      (TF32X3, "f16", 3, 16, 32), (TF32X3, "f16", 4, 16, 32),
+                                      (TF32X3, "f16", 6, 16, 32)]:
+        variants.append((f"C2 K=16 prec={prec} kind={kind} poly={poly} epi={epi} l2={l2}", src, tgt, eps, pot,
+                         prec, {"CNTGW_TC_POLY": str(poly), "CNTGW_TC_EPI": str(epi),
+                                "CNTGW_L2_CHUNK_MB": str(l2), "CNTGW_TC_KIND": kind}))
     s4, t4, e4, p4 = build(n, 3, True)
     variants.append((f"C4-law K=3+sq prec={F32}", s4, t4, e4, p4, F32, {"CNTGW_L2_CHUNK_MB": "32"}))
     for dm, nt in (("1", "0"), ("1", "2"), ("1", "11"), ("0", "0")):
