@@ -412,13 +412,17 @@ def run_b200(args, info):
     if info.rank != 0:
         return
     peaks = probe_peaks()
-    path = {F32: "fp32 FFMA2 + MUFU", F64: "fp64 DFMA + MUFU", TF32X3: "tcgen05 3xTF32 + MUFU"}[prec]
+    tc_f16 = os.environ.get("CNTGW_TC_KIND", "f16")[:1].lower() != "t"
+    path = {F32: "fp32 FFMA2 + MUFU", F64: "fp64 DFMA + MUFU",
+            TF32X3: "tcgen05 3-way split on fp16 operands + MUFU" if tc_f16 else "tcgen05 3xTF32 + MUFU"}[prec]
     if prec == TF32X3:
         # scores on the tensor cores (TMEM accumulators); the epilogue does one
-        # MUFU.EX2 per pair, so the roof is the MUFU rate
-        kp = (3 * k + 2 + 7) // 8 * 8
+        # exponential per pair, so the roof is the MUFU rate (3 of 16 pairs of
+        # exponentials run as an FMA-pipe polynomial instead)
+        kp = (3 * k + 3 + 15) // 16 * 16 if tc_f16 else (3 * k + 2 + 7) // 8 * 8
         roof, bound = peaks["ex2_per_s"], "mufu"
-        model = f"MUFU.EX2/s (1 ex2 per pair); scores: {2 * kp} tf32 flops/pair on tcgen05"
+        model = (f"MUFU.EX2/s (1 ex2 per pair); scores: {2 * kp} "
+                 f"{'f16' if tc_f16 else 'tf32'} flops/pair on tcgen05")
     else:
         # fp32 path, no sq term: FMA-pipe lane-ops per pair = K (dot) + 1
         # (exponent argument) + 1 (sum); 1 MUFU.EX2 per pair
@@ -439,7 +443,8 @@ def run_b200(args, info):
                      "peak_source": peaks["source"], "kernel_avg_ms": kern_avg_ms,
                      "pairs_per_launch": nl * m},
         "e2e": e2e,
-        "gpu_launches": args.steps * (2 * 2 + 2 * (1 if chunked else 0)),
+        # per half-update: column pack (+ the absmax pass of the fp16 operands), softmin, combine
+        "gpu_launches": args.steps * 2 * (2 + (1 if prec == TF32X3 and tc_f16 else 0) + (1 if chunked else 0)),
         "clocks": clk,
     }
     if info.world == 1 and not args.no_cpu_baseline:
@@ -570,7 +575,7 @@ def gw_solve_block(args, info, dev):
     return out
 
 
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r1_bench_traffic.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r2_bench_traffic.json")
 
 
 def ncu_traffic(tag, n, m):

@@ -145,8 +145,12 @@ int cntgw_sweep_apply(const cntgw_sweep_state* st, double* pot, const double* te
  * kernels accumulate with plain FMAs: fp32 [-2 lam z (kd) | -sqrt(lam) s (if
  * sq) | -(lam pot + log2 w) | zero pad] (squared coordinate kept as a
  * difference); fp64 [-2 lam z | -2 lam s | -(lam (pot - s^2) + log2 w)]
- * (square expanded, exact enough in fp64); tensor-core: 3xTF32 tiles (see
- * softmin_tc.cuh). Padding columns m..cols_padded(m)-1 get an exactly-zero
+ * (square expanded, exact enough in fp64); tensor-core (CNTGW_TF32X3): the
+ * 3-way split tiles of softmin_tc.cuh, on fp16 operands scaled from the
+ * absmax of the column features (default) or on tf32 operands
+ * (CNTGW_TC_KIND=tf32, read by this call and by cntgw_softmin alike); that
+ * path is for well-scaled problems, 2 lam max|x| max|z| < 2^13 (larger
+ * scores overflow fp16 and come back as inf/NaN, never silently wrong). Padding columns m..cols_padded(m)-1 get an exactly-zero
  * weight. feat: m x kd row-major (stride ld), fp32 or fp64 per
  * prec, as is sq; pot (nullable => 0) and log2w are fp64. */
 int cntgw_prep_cols(const cntgw_sweep_state* st, int prec, int kd, int sq_flag, const void* feat,

@@ -97,6 +97,7 @@ struct KernelPick {
   size_t smem;
   int threads = 128;
   size_t rec_bytes = 0;  // bytes of column records per column (L2 chunking)
+  int l2_chunk_mb = 32;  // default L2 budget of one column chunk (CNTGW_L2_CHUNK_MB overrides)
   int cta_rows = 0;      // rows per CTA when not 128 * rows
   int ctr_kx = 0;        // CNTGW_F32C FFMA2 kernel: feature width and groups per CTA
   int ctr_r = 0;         //   (block-sparse plan, ctr_plan_kernel)
@@ -174,10 +175,13 @@ KernelPick pick() {
 
 // Tensor-core variant knobs (read per call so tools can sweep them):
 // CNTGW_TC_KIND = f16 (default: the 3-way split on fp16 operands, kind::f16)
-// or tf32 (kind::tf32); CNTGW_TC_POLY in {0,2,3,4,6} (default 2, fastest in
-// tools/sweep_paths.py): pairs (of 16 per 32-column chunk) whose exp2 runs on
-// the FMA pipe instead of MUFU; CNTGW_TC_EPI in {8,16}: epilogue warps
-// (default 16).
+// or tf32 (kind::tf32); CNTGW_TC_POLY in {0,2,3,4,6} (default 3 with fp16
+// operands, 2 with tf32: fastest in tools/sweep_paths.py): pairs (of 16 per
+// 32-column chunk) whose exp2 runs on the FMA pipe instead of MUFU;
+// CNTGW_TC_EPI in {8,16}: epilogue warps (default 16). Measured slower and
+// removed: one reference check per 64 columns (both chunks loaded up front,
+// 253 vs 245 ms per C2 half-update: the next chunk's TMEM load no longer
+// overlaps the math).
 bool tc_f16() {
   const char* e = getenv("CNTGW_TC_KIND");
   return !(e && (e[0] == 't' || e[0] == 'T'));
@@ -197,9 +201,9 @@ void* tc_fn(int poly) {
 template <int KD>
 KernelPick pick_tc() {
   KernelPick k;
-  const int poly = env_int("CNTGW_TC_POLY", 2);
-  const int epi = env_int("CNTGW_TC_EPI", 16) == 8 ? 8 : 16;
   const bool h = tc_f16();
+  const int poly = env_int("CNTGW_TC_POLY", h ? 3 : 2);
+  const int epi = env_int("CNTGW_TC_EPI", 16) == 8 ? 8 : 16;
   if (h) k.fn = epi == 16 ? tc_fn<KD, 16, true>(poly) : tc_fn<KD, 8, true>(poly);
   else k.fn = epi == 16 ? tc_fn<KD, 16, false>(poly) : tc_fn<KD, 8, false>(poly);
   k.rows = 1;  // 128 rows per CTA = 128 threads x 1 in the planner's units
@@ -207,6 +211,9 @@ KernelPick pick_tc() {
   const size_t b_bytes = h ? TcLayoutH<KD>::kBTileBytes : TcLayout<KD>::kBTileBytes;
   k.smem = a_bytes + kTcStages * b_bytes;
   k.rec_bytes = h ? TcLayoutH<KD>::kRecBytes : TcLayout<KD>::kRecBytes;
+  // C2 2^20 per half-update: 48 MB chunks 245.1 ms / 0.45 GB of DRAM traffic, 32 MB 245.5 ms /
+  // 0.48 GB, 64 MB 243.2 ms / 3.5 GB (past the L2's effective capacity), unchunked 243.9 ms
+  k.l2_chunk_mb = 48;
   k.threads = tc_threads(epi);
   return k;
 }
@@ -479,7 +486,7 @@ Plan plan_softmin(int64_t n, int64_t m, const KernelPick& k) {
   // Keeping a chunk's records within an L2 budget turns the re-reads of
   // 8000+ row tiles into L2 hits instead of DRAM misses (B' for N = 2^20,
   // K = 16 is 235 MB against a 126 MB L2).
-  const int64_t budget = (int64_t)env_int("CNTGW_L2_CHUNK_MB", 32) << 20;
+  const int64_t budget = (int64_t)env_int("CNTGW_L2_CHUNK_MB", k.l2_chunk_mb) << 20;
   int64_t min_c = 1;
   if (budget > 0 && k.rec_bytes > 0) {
     const int64_t tile_bytes = (int64_t)k.rec_bytes * kColTile;

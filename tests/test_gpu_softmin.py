@@ -289,13 +289,17 @@ def test_c2_full_size_g_update_given_gpu_f(env, c2_full):
     assert _rel(res.coupling.g[cols], want) < 1e-5
 
 
-@pytest.mark.parametrize("prec", [0, 2], ids=["f32", "tc"])
+@pytest.mark.parametrize("prec,kind", [(0, None), (2, "f16"), (2, "tf32")], ids=["f32", "tc-f16", "tc-tf32"])
 @pytest.mark.parametrize("k", [8, 16])
 @pytest.mark.parametrize("n,m", [(1, 1), (129, 257), (1000, 1000), (2049, 771), (300, 5000)])
-def test_low_rank_paths(env, prec, k, n, m):
-    """fp32 FFMA2 and tcgen05 3xTF32 half-updates on the C2 cost form."""
+def test_low_rank_paths(env, prec, kind, k, n, m, monkeypatch):
+    """fp32 FFMA2 and tcgen05 split-precision half-updates (fp16 operands, the
+    default, and tf32 operands) on the C2 cost form."""
     P, engine, S, O, torch, dev = env
     from paper_2602_06658_b200 import configs
+
+    if kind:
+        monkeypatch.setenv("CNTGW_TC_KIND", kind)
 
     inst = configs.c2(seed=n + m + k, n=n, m=m, k=k)
     a, b = np.full(n, 1 / n), np.full(m, 1 / m)
@@ -303,6 +307,38 @@ def test_low_rank_paths(env, prec, k, n, m):
     got = _half_update(env, cost, a, b, inst.g.astype(float) + inst.col_sep, inst.eps, prec)
     want = O.softmin(O.LowRank(inst.u, inst.v, inst.row_sep, inst.col_sep), np.log(b),
                      inst.g.astype(float) + inst.col_sep, inst.eps)
+    assert _rel(got, want) < 1e-5
+
+
+@pytest.mark.parametrize("k", [8, 16])
+@pytest.mark.parametrize("shift", [0, 30, -30])
+@pytest.mark.parametrize("poly", ["0", "3", "6"])
+def test_tc_fp16_operand_ranges(env, k, shift, poly, monkeypatch):
+    """The fp16-operand tcgen05 split scales both sides into fp16's exponent
+    range from the absmax of the column features: the same scores with the
+    features scaled by 2^s / 2^-s, features 2^-20 / 2^-25 below the side's
+    largest (values below fp16's normal range after scaling), zero-weight columns
+    (log2 w = -inf) and a large bias all match the oracle; every split of the
+    exponentials between MUFU and the FMA pipe."""
+    P, engine, S, O, torch, dev = env
+    monkeypatch.setenv("CNTGW_TC_KIND", "f16")
+    monkeypatch.setenv("CNTGW_TC_POLY", poly)
+    rng = np.random.default_rng(100 + k + shift)
+    n, m = 700, 1500
+    u = (rng.standard_normal((n, k)) * 0.25 * 2.0 ** shift).astype(np.float32)
+    v = (rng.standard_normal((m, k)) * 0.25 * 2.0 ** -shift).astype(np.float32)
+    v[:, k // 2:] *= np.float32(2.0 ** -20)  # half of the products vanish against the rest
+    u[:, :k // 4] *= np.float32(2.0 ** -25)
+    a = np.full(n, 1 / n)
+    b = np.where(np.arange(m) % 7 == 3, 0.0, 1.0)
+    b /= b.sum()
+    g = rng.standard_normal(m) * 40.0  # |bias| ~ 1e3 log2 units at eps = 0.05
+    zero_n, zero_m = np.zeros(n), np.zeros(m)
+    cost = P.SeparableLowRankCost(u, v, zero_n, zero_m)
+    with np.errstate(divide="ignore"):
+        want = O.softmin(O.LowRank(u, v, zero_n, zero_m), np.log(b), g, 0.05)
+    got = _half_update(env, cost, a, b, g, 0.05, 2)
+    assert np.all(np.isfinite(got))
     assert _rel(got, want) < 1e-5
 
 

@@ -59,9 +59,9 @@ def main(n=1 << 19, reps=3, rounds=3, only=None):
                                       (TF32X3, "tf32", 2, 16, 32), (TF32X3, "tf32", 2, 16, 0),
                                       (TF32X3, "tf32", 4, 16, 32), (TF32X3, "f16", 0, 16, 32),
                                       (TF32X3, "f16", 2, 8, 32), (TF32X3, "f16", 2, 16, 32),
-                                      (TF32X3, "f16", 2, 16, 0), (TF32X3, "f16", 2, 16, 64),
-                                      (TF32X3, "f16", 3, 16, 32), (TF32X3, "f16", 4, 16, 32),
-                                      (TF32X3, "f16", 6, 16, 32)]:
+                                      (TF32X3, "f16", 3, 16, 32), (TF32X3, "f16", 3, 16, 64),
+                                      (TF32X3, "f16", 3, 16, 0), (TF32X3, "f16", 4, 16, 64),
+                                      (TF32X3, "f16", 6, 16, 64)]:
         variants.append((f"C2 K=16 prec={prec} kind={kind} poly={poly} epi={epi} l2={l2}", src, tgt, eps, pot,
                          prec, {"CNTGW_TC_POLY": str(poly), "CNTGW_TC_EPI": str(epi),
                                 "CNTGW_L2_CHUNK_MB": str(l2), "CNTGW_TC_KIND": kind}))
