@@ -294,6 +294,7 @@ struct F64sPlan {
   int* nan;        // the probe stands down (non-finite records)
   int* probe_ok;   // this sweep's plan came from the probe
   float* slack;    // the probe's 2 max E (log2 units)
+  int* sched;      // re-measurement schedule: interval, kept pairs before the last one, pending, its sweep
   float* rec32;    // fp32 probe records [mpad][P]
   float* sbound;   // per stage magnitude bounds [stages][P]
 };
@@ -315,10 +316,16 @@ F64sPlan f64s_plan(void* base_v, const F64sPlanLayout& l) {
   p.nan = p.counter + 3;
   p.probe_ok = p.counter + 4;
   p.slack = reinterpret_cast<float*>(p.counter + 5);
+  p.sched = p.counter + 6;
   char* tail = base + l.tmin + l.need + l.cplan + l.range + l.gmin + l.tstar + l.rowmin + 256;
   p.rec32 = l.rec32 ? reinterpret_cast<float*>(tail) : nullptr;
   p.sbound = l.sbound ? reinterpret_cast<float*>(tail + l.rec32) : nullptr;
   return p;
+}
+
+// f64s_reduce_kernel: two row-minimum arrays + the walked-stage list (uint16)
+size_t f64s_reduce_smem(const KernelPick& k, int stages) {
+  return 2 * sizeof(double) * k.cta_rows + (stages <= kF64sListMax ? sizeof(uint16_t) * (size_t)stages : 0);
 }
 
 // Re-vote the measured plan for the current records (f64s_* kernels,
@@ -332,20 +339,24 @@ int f64s_vote(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl, 
                                                                        : (kd + sq + 3) / 4 * 4;
   f64s_shift_kernel<<<(unsigned)l.stages, 128, 0, s>>>(rec, stride, kd + sq, m, k.f64s_tile, pl.c_plan, pl.range,
                                                         pl.flag, pl.full, gate);
+  // Sweeps skip terms below 2^-48 of their row's maximum: the skipped mass, < m 2^-48 of the row
+  // sum, stays 16x under the fp32 rounding (2^-24) of the kernel's per-stage partial sums at
+  // m = 2^20. The plan consumers (K4: fp64 exponentials and sums, schedule == 0) keep 2^-64.
   const char* te = getenv("CNTGW_CTR_SKIP_T");
-  const double T = te ? atof(te) : 64.0;
+  const double T = te ? atof(te) : (schedule ? 48.0 : 64.0);
   f64s_vote_kernel<<<(unsigned)l.row_tiles, 256, 0, s>>>(pl.flag, pl.gmin, pl.tstar, pl.range, n, l.stages,
                                                          k.cta_rows, T, pl.need, pl.counter, gate);
   const char* fe = getenv("CNTGW_F64S_REMEASURE");
   const double frac = fe ? atof(fe) : 0.25;
   f64s_decide_kernel<<<1, 1, 0, s>>>(st, pl.flag, pl.counter, pl.next_measure, l.row_tiles * (int64_t)l.stages,
-                                     frac, schedule, gate, skip);
+                                     frac, schedule, gate, skip, pl.sched, pl.full,
+                                     k.probe_fn != nullptr && env_int("CNTGW_F64S_PROBE", 1) != 0 ? 1 : 0);
   return check_launch("f64s_vote");
 }
 int f64s_revote(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl, const cntgw_sweep_state* st,
                 const double* rec, int kd, int sq, const void* rows, const void* cols, int64_t n, int64_t m,
                 cudaStream_t s, int schedule, int skip) {
-  f64s_begin_kernel<<<1, 1, 0, s>>>(st, skip, pl.key, rows, cols, n, m, pl.flag, pl.counter, pl.full);
+  f64s_begin_kernel<<<1, 1, 0, s>>>(st, skip, pl.key, rows, cols, n, m, pl.flag, pl.counter, pl.full, pl.sched);
   return f64s_vote(k, l, pl, st, rec, kd, sq, n, m, s, schedule, nullptr, skip);
 }
 
@@ -387,11 +398,11 @@ int f64s_probe(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl,
       return fail(CNTGW_ECUDA, "f64s probe: %s", cudaGetErrorString(e));
     }
   }
-  f64s_reduce_kernel<<<(unsigned)l.row_tiles, 256, 2 * sizeof(double) * k.cta_rows, s>>>(
+  f64s_reduce_kernel<<<(unsigned)l.row_tiles, 256, f64s_reduce_smem(k, l.stages), s>>>(
       pl.probe_ok, pl.probe_ok, pl.tmin, pl.need, pl.range, n, l.stages, k.cta_rows, pl.gmin, pl.tstar, pl.rowmin,
       0.f, pl.slack);
   f64s_commit_kernel<<<1, 1024, 0, s>>>(pl.probe_ok, st, rec, stride, kd + sq, mpad, pl.c_plan, pl.key, rows, cols,
-                                        n, m, pl.next_measure);
+                                        n, m, pl.next_measure, pl.counter, pl.sched);
   f64s_probed_kernel<<<1, 1, 0, s>>>(pl.probe_ok, pl.flag, pl.full, pl.counter);
   return f64s_vote(k, l, pl, st, rec, kd, sq, n, m, s, 1, pl.probe_ok, skip);
 }
@@ -932,7 +943,7 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
                                    skip_if_done))
       return rc;
     if (env_int("CNTGW_CTR_REUSE", 1) == 0) f64s_begin_kernel<<<1, 1, 0, s>>>(nullptr, 0, pl.key, row_feat, col_rec,
-                                                                                n, m, pl.flag, pl.counter, pl.full);
+                                                                                n, m, pl.flag, pl.counter, pl.full, pl.sched);
     if (f64s_probe_enabled(k))
       if (const int rc = f64s_probe(k, fl, pl, st, skip_if_done, rec, kd, sq_flag ? 1 : 0, row_feat, col_rec, n, m, s))
         return rc;
@@ -944,12 +955,12 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
       return fail(CNTGW_ECUDA, "softmin f64s launch: %s", cudaGetErrorString(e2));
     }
     const int64_t mpad = (m + kColTile - 1) / kColTile * kColTile;
-    f64s_reduce_kernel<<<(unsigned)fl.row_tiles, 256, 2 * sizeof(double) * k.cta_rows, s>>>(
+    f64s_reduce_kernel<<<(unsigned)fl.row_tiles, 256, f64s_reduce_smem(k, fl.stages), s>>>(
         pl.flag, pl.full, pl.tmin, pl.need, pl.range, n, fl.stages, k.cta_rows, pl.gmin, pl.tstar, pl.rowmin,
         0.f, nullptr);  // (the fp64 kernel measures exact stage minima: no slack)
     f64s_commit_kernel<<<1, 1024, 0, s>>>(pl.flag, st, rec, cntgw_col_stride(CNTGW_F64S, kd, sq_flag),
                                           kd + (sq_flag ? 1 : 0), mpad, pl.c_plan, pl.key, row_feat, col_rec, n, m,
-                                          pl.next_measure);
+                                          pl.next_measure, pl.counter, pl.sched);
     if (const int rc = check_launch("f64s_commit")) return rc;
     if (p.nchunks > 1) {
       const int th = 256;

@@ -21,8 +21,9 @@
 //     f64s_vote kernels, below) and walks only the needed stages (their
 //     compacted list is built in shared memory, so the bulk-copy ring stays
 //     dense).
-// Skipped terms are below 2^-64 of their row's maximum (exact bounds, no
-// assumption on how the potentials move), so the skipped mass is < m 2^-64
+// Skipped terms are below 2^-48 of their row's maximum in the sweeps (2^-64
+// for the plan consumers; exact bounds, no assumption on how the potentials
+// move), so the skipped mass is < m 2^-48
 // of every row's sum. On the C5 law 8% of the (row group, stage) pairs are
 // needed right after a measurement (tools/c5_sparsity.py).
 #pragma once
@@ -98,7 +99,8 @@ __global__ void select_order_kernel(const double* gamma, int de, const int64_t* 
 
 // (1 block) replan = first sweep / new key; the counter of needed pairs = 0
 __global__ void f64s_begin_kernel(const cntgw_sweep_state* st, int skip, CtrPlanKey* key, const void* rows,
-                                  const void* cols, int64_t n, int64_t m, int* flag, int* counter, int* full) {
+                                  const void* cols, int64_t n, int64_t m, int* flag, int* counter, int* full,
+                                  int* sched) {
   if (skip_now(st, skip)) {  // (the loop is done: no sweep, no measurement)
     *flag = 0;
     *full = 0;
@@ -111,6 +113,10 @@ __global__ void f64s_begin_kernel(const cntgw_sweep_state* st, int skip, CtrPlan
   *flag = first ? 1 : 0;
   *full = first ? 1 : 0;  // a measurement over every stage (else: over the kept ones)
   *counter = 0;
+  if (first) {  // a new plan: the re-measurement schedule starts over
+    sched[0] = 1;
+    sched[2] = 0;
+  }
 }
 
 // one block per stage: the range of the column shifts over the stage's real
@@ -166,24 +172,56 @@ __global__ void __launch_bounds__(128) f64s_shift_kernel(const double* rec, int 
 // keeps the re-vote's lower bound of its minimum, Mq_i(old) + gmin(old) +
 // dmin_t (valid in the current frame, and > the row minimum + T), so the new
 // plan stays a plan of lower bounds.
+constexpr int kF64sListMax = 16384;  // walked-stage list held in shared memory (32 KB)
 __global__ void __launch_bounds__(256) f64s_reduce_kernel(const int* flag, const int* full, const float* tmin,
                                                           const uint8_t* need, const double2* range, int64_t n,
                                                           int stages, int grows, float* gmin, int* tstar,
                                                           double* rowmin, float slack_c, const float* slack_p) {
   if (!*flag) return;
   const bool all = *full != 0;
-  extern __shared__ double rsh[];  // [grows] new row minima | [grows] previous ones
+  // dynamic: [grows] new row minima | [grows] previous ones | [stages] uint16 walked-stage list
+  extern __shared__ double rsh[];
+  __shared__ int wsum[8];
+  __shared__ int nwalk_s;
+  __shared__ double dmin_s;
   double* rnew = rsh;
   double* rold = rsh + grows;
+  uint16_t* walk = reinterpret_cast<uint16_t*>(rsh + 2 * grows);
   const int64_t r0 = (int64_t)blockIdx.x * grows;
   const uint8_t* nd = need + (int64_t)blockIdx.x * stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // a partial measurement walked only the kept stages (a few per group): their
+  // compacted list, so that the per-row scans below do not visit every stage
+  const bool listed = !all && stages <= kF64sListMax;
+  if (listed) {
+    const int per = (stages + (int)blockDim.x - 1) / (int)blockDim.x;
+    const int first = (int)threadIdx.x * per;
+    int cnt = 0;
+    for (int u = 0; u < per; ++u)
+      if (first + u < stages && nd[first + u]) ++cnt;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int pos = incl - cnt;
+    for (int w = 0; w < warp; ++w) pos += wsum[w];
+    for (int u = 0; u < per; ++u)
+      if (first + u < stages && nd[first + u]) walk[pos++] = (uint16_t)(first + u);
+    if (threadIdx.x == blockDim.x - 1) nwalk_s = pos;
+    __syncthreads();
+  }
+  const int nwalk = listed ? nwalk_s : stages;
   for (int r = warp; r < grows; r += nw) {
     float mn = CUDART_INF_F;
     int at = 0;
     if (r0 + r < n)
-      for (int t = lane; t < stages; t += 32) {
-        if (!all && !nd[t]) continue;
+      for (int k = lane; k < nwalk; k += 32) {
+        const int t = listed ? (int)walk[k] : k;
+        if (!all && !listed && !nd[t]) continue;
         const float v = tmin[(r0 + r) * stages + t];
         if (v < mn) {
           mn = v;
@@ -213,13 +251,24 @@ __global__ void __launch_bounds__(256) f64s_reduce_kernel(const int* flag, const
   for (int r = 0; r < grows && r0 + r < n; ++r)
     if (fabs(rnew[r]) < CUDART_INF) amax = fmax(amax, fabs(rnew[r]));
   const double allow = amax * 0x1p-22 + (slack_p ? (double)*slack_p : (double)slack_c);
+  // a stage the measurement skipped keeps the re-vote's bound: over the rows,
+  // min (rold + gold - rnew) = gold + min (rold - rnew), the same for every such stage
+  if (warp == 0) {
+    double dm = CUDART_INF;
+    for (int r = lane; r < grows && r0 + r < n; r += 32) dm = fmin(dm, rold[r] - rnew[r]);  // (NaN dropped)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dm = fmin(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+    if (lane == 0) dmin_s = dm;
+  }
+  __syncthreads();
+  const double dmin = dmin_s;
   for (int t = threadIdx.x; t < stages; t += blockDim.x) {
-    const bool walked = all || nd[t];
-    const double gold = walked ? 0.0 : (double)gmin[(int64_t)blockIdx.x * stages + t] + range[t].x;
     double g = CUDART_INF;
-    for (int r = 0; r < grows && r0 + r < n; ++r) {
-      const double v = walked ? (double)tmin[(r0 + r) * stages + t] : rold[r] + gold;
-      g = fmin(g, v - rnew[r]);  // (inf - inf: an empty row, NaN dropped)
+    if (all || nd[t]) {
+      for (int r = 0; r < grows && r0 + r < n; ++r)
+        g = fmin(g, (double)tmin[(r0 + r) * stages + t] - rnew[r]);  // (inf - inf: an empty row, NaN dropped)
+    } else {
+      g = dmin + ((double)gmin[(int64_t)blockIdx.x * stages + t] + range[t].x);
     }
     gmin[(int64_t)blockIdx.x * stages + t] = __double2float_rd(g - allow);
   }
@@ -261,18 +310,34 @@ __global__ void __launch_bounds__(256) f64s_vote_kernel(const int* flag, const f
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(counter, cnt);
 }
 
-// (1 thread) measure anew when the re-vote kept too much, and on a schedule
-// (every sweep up to the 8th, then 16, 32, ...) while it keeps more than
-// 0.2%: a plan measured early in a loop reflects transient potentials, and
-// the re-vote only ever loosens it. Within a loop a measurement walks only the
-// kept stages (~1.3 sparse sweeps); the first one of a loop is dense.
+// (1 thread) measure anew when the re-vote kept too much, and on an adaptive
+// schedule while it keeps more than 0.2%: a plan measured early in a loop
+// reflects transient potentials, and the re-vote only ever loosens it. Within
+// a loop a measurement walks only the kept stages (~1.3-2 sparse sweeps); the
+// first one of a loop is dense (or the fp32 probe). The first vote after a
+// measurement tells whether it paid: if it cut the kept pairs by more than 5%
+// the interval to the next measurement halves (down to the very next sweep),
+// otherwise it doubles (sched: interval, kept pairs before the last
+// measurement, pending flag, sweep of the last measurement).
 __global__ void f64s_decide_kernel(const cntgw_sweep_state* st, int* flag, const int* counter,
-                                   const int* next_measure, int64_t pairs, double max_frac, int schedule,
-                                   const int* gate, int skip) {
+                                   int* next_measure, int64_t pairs, double max_frac, int schedule,
+                                   const int* gate, int skip, int* sched, int* full, int reprobe) {
   if (*flag || (gate && !*gate) || skip_now(st, skip)) return;
   const double kept = (double)*counter / (double)pairs;
   const int sweep = st ? st->sweep : 0;
+  if (schedule && sched[2]) {
+    sched[2] = 0;
+    const int before = sched[1];
+    const bool paid = before <= 0 || (double)(before - *counter) > 0.05 * (double)before;
+    const int prev = sched[0] > 1 ? sched[0] : 1;
+    sched[0] = paid ? (prev > 2 ? prev / 2 : 1) : (prev < 32768 ? 2 * prev : prev);
+    *next_measure = sched[3] + sched[0];
+  }
   if (kept > max_frac || (schedule && sweep >= *next_measure && kept > 0.002)) *flag = 1;
+  // the re-vote lost the plan (potentials moved far, e.g. the second sweep from
+  // zero potentials keeps 99%): where the fp32 probe exists, a fresh probe
+  // (0.3 dense sweeps) beats walking that much in fp64
+  if (reprobe && schedule && !gate && kept > max_frac) *full = 1;
 }
 
 // diagnostics: needed (group, stage) pairs of the current mask and the flag
@@ -295,14 +360,16 @@ __global__ void __launch_bounds__(1024) f64s_commit_kernel(const int* flag, cons
                                                            const double* rec, int stride, int off, int64_t mpad,
                                                            double* c_plan, CtrPlanKey* key, const void* rows,
                                                            const void* cols, int64_t n, int64_t m,
-                                                           int* next_measure) {
+                                                           int* next_measure, const int* counter, int* sched) {
   if (!*flag) return;
   for (int64_t j = threadIdx.x; j < mpad; j += blockDim.x) c_plan[j] = rec[j * stride + off];
   if (threadIdx.x == 0) {
     const int sweep = st ? st->sweep : 0;
-    // partial re-measurements cost ~1.3 sparse sweeps: every sweep while the
-    // early potentials move fast, then at sweeps 16, 32, 64, ...
-    *next_measure = sweep < 8 ? sweep + 1 : 2 * sweep;
+    // the next vote decides when to measure again (f64s_decide_kernel)
+    *next_measure = sweep + 1;
+    sched[1] = *counter;  // kept pairs of the vote this measurement followed (0: a first, dense one)
+    sched[2] = 1;
+    sched[3] = sweep;
     key->lam = st ? st->lam_d : 0.0;
     key->rows = rows;
     key->cols = cols;
@@ -404,25 +471,35 @@ __global__ void __launch_bounds__(128, MINB) softmin_f64s_kernel(const SoftminAr
   const int64_t mpad = (a.m + kColTile - 1) / kColTile * kColTile;
   const int ntiles = (int)((min(c0 + a.chunk_cols, mpad) - c0) / TILE);
   const int t0 = (int)(c0 / TILE);  // global stage index of the chunk's first stage
-  // compacted list of the stages this CTA walks (all of them on a replan sweep)
-  if (threadIdx.x == 0) nlist = 0;
-  __syncthreads();
+  // compacted list of the stages this CTA walks (all of them on a full
+  // measuring sweep), in increasing order: every thread takes a contiguous run
+  // of <= 32 stages (its mask bytes are independent loads, one L2 round trip
+  // for the CTA), and a block prefix sum of the counts places the runs
   {
+    __shared__ int wsum[4];
     const uint8_t* nd = p.need + (int64_t)blockIdx.x * p.stages + t0;
-    for (int base = 0; base < ntiles; base += blockDim.x) {
-      const int t = base + threadIdx.x;
-      const bool take = t < ntiles && (full || nd[t]);
-      const unsigned ball = __ballot_sync(0xffffffffu, take);
-      // warp-ordered append: keep the stages in increasing order
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-        if (warp == w && lane == 0 && ball) {
-          int pos = nlist;
-          for (unsigned b = ball; b; b &= b - 1) list[pos++] = (int16_t)(base + 32 * w + __ffs(b) - 1);
-          nlist = pos;
-        }
-        __syncthreads();
-      }
+    const int per = (ntiles + (int)blockDim.x - 1) / (int)blockDim.x;  // <= kMaxList / 128
+    const int first = (int)threadIdx.x * per;
+    uint32_t mask = 0;
+#pragma unroll 8
+    for (int u = 0; u < per; ++u) {
+      const int t = first + u;
+      if (t < ntiles && (full || nd[t])) mask |= 1u << u;
     }
+    const int cnt = __popc(mask);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int pos = incl - cnt;
+    for (int w = 0; w < warp; ++w) pos += wsum[w];
+    for (uint32_t b = mask; b; b &= b - 1) list[pos++] = (int16_t)(first + __ffs(b) - 1);
+    if (threadIdx.x == blockDim.x - 1) nlist = pos;
+    __syncthreads();
   }
   const int nt = nlist;
   const uint32_t bytes = kStage * sizeof(double);
