@@ -13,6 +13,7 @@
 #include "softmin_dmma.cuh"
 #include "softmin_f64s.cuh"
 #include "softmin_f64s_probe.cuh"
+#include "softmin_f64s_tcprobe.cuh"
 #include "reduce_ctr.cuh"
 #include "softmin_tc.cuh"
 #include "sweep.cuh"
@@ -105,7 +106,13 @@ struct KernelPick {
   void* probe_fn = nullptr;  // CNTGW_F64S, kd + sq <= 8: the fp32 probe of a dense measurement
   void* probe_prep_fn = nullptr;
   int probe_rows = 0;        //   rows per probe CTA (128 threads x R)
-  int probe_p = 0;           //   floats per fp32 probe record
+  int probe_p = 0;           //   floats per probe record (fp32 record / fp16 stage tile column)
+  void* tcp_fn = nullptr;        // CNTGW_F64S: the tcgen05 probe (softmin_f64s_tcprobe.cuh), any width
+  void* tcp_stats_fn = nullptr;
+  void* tcp_pack_fn = nullptr;
+  int tcp_threads = 0;
+  size_t tcp_smem = 0;
+  size_t tcp_stage_bytes = 0;
 };
 
 // CNTGW_F64S: the DMMA kernel's tiling (same choices as pick<F64>) on ordered
@@ -127,6 +134,17 @@ KernelPick pick_f64s() {
     k.probe_prep_fn = (void*)f64s_probe_prep_kernel<KD + SQ>;
     k.probe_rows = 128 * R;
     k.probe_p = ProbeLayout<KD + SQ>::kP;
+  }
+  {
+    using TL = TcpLayout<KD + SQ>;
+    constexpr int NB = 512 / TD < 4 ? 512 / TD : 4;
+    k.tcp_fn = (void*)f64s_tcp_kernel<KD + SQ, TD>;
+    k.tcp_stats_fn = (void*)f64s_tcp_stats_kernel<KD + SQ>;
+    k.tcp_pack_fn = (void*)f64s_tcp_pack_kernel<KD + SQ>;
+    k.tcp_threads = 64 + 128 * NB;
+    k.tcp_stage_bytes = (size_t)TL::kChunks * TD * 16;
+    k.tcp_smem = (size_t)TL::kATileBytes + kTcpStages * k.tcp_stage_bytes;
+    if (TL::kP > k.probe_p) k.probe_p = TL::kP;
   }
   return k;
 }
@@ -270,8 +288,8 @@ F64sPlanLayout f64s_layout(const KernelPick& k, int64_t n, int64_t m) {
   l.gmin = align256(sizeof(float) * (size_t)l.row_tiles * l.stages);
   l.tstar = align256(sizeof(int) * (size_t)n);
   l.rowmin = align256(sizeof(double) * (size_t)n);
-  l.rec32 = k.probe_fn ? align256(sizeof(float) * (size_t)mpad * k.probe_p) : 0;
-  l.sbound = k.probe_fn ? align256(sizeof(float) * (size_t)l.stages * k.probe_p) : 0;
+  l.rec32 = k.probe_p ? align256(sizeof(float) * (size_t)mpad * k.probe_p) : 0;
+  l.sbound = k.probe_p ? std::max(align256(sizeof(float) * (size_t)l.stages * k.probe_p), tcp_bounds_bytes(l.stages)) : 0;
   l.total = l.tmin + l.need + l.cplan + l.range + l.gmin + l.tstar + l.rowmin + 256 + l.rec32 + l.sbound;
   // (the 256 bytes after rowmin: CtrPlanKey, flags)
   return l;
@@ -323,6 +341,14 @@ F64sPlan f64s_plan(void* base_v, const F64sPlanLayout& l) {
   return p;
 }
 
+// CNTGW_F64S_PROBE=0: dense fp64 measurements; CNTGW_F64S_PROBE_TC=0: the FFMA2 probe (kd + sq <= 8)
+bool f64s_tcp_enabled(const KernelPick& k) {
+  return k.tcp_fn != nullptr && env_int("CNTGW_F64S_PROBE", 1) != 0 && env_int("CNTGW_F64S_PROBE_TC", 1) != 0;
+}
+bool f64s_probe_enabled(const KernelPick& k) {
+  return (k.probe_fn != nullptr || f64s_tcp_enabled(k)) && env_int("CNTGW_F64S_PROBE", 1) != 0;
+}
+
 // f64s_reduce_kernel: two row-minimum arrays + the walked-stage list (uint16)
 size_t f64s_reduce_smem(const KernelPick& k, int stages) {
   return 2 * sizeof(double) * k.cta_rows + (stages <= kF64sListMax ? sizeof(uint16_t) * (size_t)stages : 0);
@@ -350,7 +376,7 @@ int f64s_vote(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl, 
   const double frac = fe ? atof(fe) : 0.25;
   f64s_decide_kernel<<<1, 1, 0, s>>>(st, pl.flag, pl.counter, pl.next_measure, l.row_tiles * (int64_t)l.stages,
                                      frac, schedule, gate, skip, pl.sched, pl.full,
-                                     k.probe_fn != nullptr && env_int("CNTGW_F64S_PROBE", 1) != 0 ? 1 : 0);
+                                     f64s_probe_enabled(k) ? 1 : 0);
   return check_launch("f64s_vote");
 }
 int f64s_revote(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl, const cntgw_sweep_state* st,
@@ -370,6 +396,51 @@ int f64s_probe(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl,
   const int stride = cntgw_col_stride(CNTGW_F64S, kd, sq);
   const int64_t mpad = (m + kColTile - 1) / kColTile * kColTile;
   cudaMemsetAsync(pl.nan, 0, sizeof(int), s);
+  if (f64s_tcp_enabled(k)) {  // the tensor-core probe (softmin_f64s_tcprobe.cuh)
+    int stages = l.stages;
+    __half* tiles = reinterpret_cast<__half*>(pl.rec32);
+    f64s_tcp_begin_kernel<<<1, 1, 0, s>>>(pl.sbound, stages);
+    {
+      void* args[] = {(void*)&pl.full, (void*)&rec,       (void*)&stride, (void*)&m,
+                      (void*)&k.f64s_tile, (void*)&pl.sbound, (void*)&stages, (void*)&pl.nan};
+      const cudaError_t e = cudaLaunchKernel(k.tcp_stats_fn, dim3(l.stages), dim3(128), args, 0, s);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CNTGW_ECUDA, "f64s tc probe stats: %s", cudaGetErrorString(e));
+      }
+    }
+    f64s_tcp_rows_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1184), 256, 0, s>>>(
+        pl.full, rows, n, kd, sq, pl.sbound, stages, pl.nan);
+    f64s_probe_gate_kernel<<<1, 1, 0, s>>>(pl.full, pl.nan, pl.probe_ok, pl.slack);
+    f64s_tcp_scales_kernel<<<1, 1, 0, s>>>(pl.probe_ok, pl.sbound, stages);
+    {
+      void* args[] = {(void*)&pl.probe_ok, (void*)&rec,   (void*)&stride,    (void*)&m,
+                      (void*)&k.f64s_tile, (void*)&tiles, (void*)&pl.sbound, (void*)&stages};
+      const cudaError_t e = cudaLaunchKernel(k.tcp_pack_fn, dim3(l.stages), dim3(128), args, 0, s);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CNTGW_ECUDA, "f64s tc probe pack: %s", cudaGetErrorString(e));
+      }
+    }
+    {
+      // stage tiles in chunks of <= 48 MB (L2), at least ~2 waves of CTAs
+      const int64_t rt = (n + kTcRows - 1) / kTcRows;
+      const int64_t fit = std::max<int64_t>(1, ((int64_t)48 << 20) / (int64_t)k.tcp_stage_bytes);
+      int chunks = (int)((l.stages + fit - 1) / fit);
+      chunks = (int)std::max<int64_t>(chunks, std::min<int64_t>(l.stages, (2 * num_sms() + rt - 1) / rt));
+      const int cs = (l.stages + chunks - 1) / chunks;
+      chunks = (l.stages + cs - 1) / cs;
+      cudaFuncSetAttribute(k.tcp_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.tcp_smem);
+      void* args[] = {(void*)&pl.probe_ok, (void*)&rows,   (void*)&n,  (void*)&kd,      (void*)&tiles,
+                      (void*)&pl.sbound,   (void*)&stages, (void*)&cs, (void*)&pl.tmin, (void*)&pl.slack};
+      const cudaError_t e =
+          cudaLaunchKernel(k.tcp_fn, dim3((unsigned)rt, (unsigned)chunks), dim3(k.tcp_threads), args, k.tcp_smem, s);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CNTGW_ECUDA, "f64s tc probe: %s", cudaGetErrorString(e));
+      }
+    }
+  } else {
   {
     void* args[] = {(void*)&pl.full, (void*)&rec, (void*)&stride, (void*)&m, (void*)&k.f64s_tile,
                     (void*)&pl.rec32, (void*)&pl.sbound, (void*)&pl.nan};
@@ -398,6 +469,7 @@ int f64s_probe(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl,
       return fail(CNTGW_ECUDA, "f64s probe: %s", cudaGetErrorString(e));
     }
   }
+  }
   f64s_reduce_kernel<<<(unsigned)l.row_tiles, 256, f64s_reduce_smem(k, l.stages), s>>>(
       pl.probe_ok, pl.probe_ok, pl.tmin, pl.need, pl.range, n, l.stages, k.cta_rows, pl.gmin, pl.tstar, pl.rowmin,
       0.f, pl.slack);
@@ -406,7 +478,6 @@ int f64s_probe(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl,
   f64s_probed_kernel<<<1, 1, 0, s>>>(pl.probe_ok, pl.flag, pl.full, pl.counter);
   return f64s_vote(k, l, pl, st, rec, kd, sq, n, m, s, 1, pl.probe_ok, skip);
 }
-bool f64s_probe_enabled(const KernelPick& k) { return k.probe_fn != nullptr && env_int("CNTGW_F64S_PROBE", 1) != 0; }
 size_t f64s_plan_bytes(const KernelPick& k, int64_t n, int64_t m) { return f64s_layout(k, n, m).total; }
 
 // CNTGW_F32C, kx <= 4, on tcgen05 (softmin_ctr_tc.cuh), opt-in with CNTGW_CTR_TC=1:

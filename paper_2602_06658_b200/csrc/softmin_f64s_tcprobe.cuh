@@ -1,0 +1,384 @@
+// CNTGW_F64S: the plan probe on the 5th-generation tensor cores.
+//
+// Same job as the FFMA2 probe (softmin_f64s_probe.cuh): lower bounds of each
+// row's minimum q_ij = beta_j + sum_k a_ik b_jk over every column stage, with
+// a rigorous error bound, so that the exact fp64 sweep that follows walks only
+// the stages a plan built from them keeps. Here the scores are a
+// split-precision tcgen05 MMA on fp16 operands (the C2 kernel's operand
+// format, softmin_tc.cuh: hi = tf32(x), lo = tf32(x - hi) have 11 significant
+// bits, exactly fp16's) into TMEM accumulators, and the epilogue is one FMNMX3
+// per two columns: no exponentials, no per-pair FMAs on the CUDA cores. Any
+// width kd + sq <= 65 (the FFMA2 probe stops at 8: C5 had none).
+//
+// Scaling (f64s_tcp_scales): with 2^ea > max |a|, 2^eb > max |b|,
+// 2^ebeta > max finite |beta| over the whole side, the accumulator holds
+// q * 2^esig, esig = min(28 - ea - eb, 29 - ebeta); rows are stored as
+// a * 2^(14 - ea) (|.| < 2^14), columns as b * 2^(esig - 14 + ea)
+// (|.| <= 2^14), the bias as three fp16 parts of beta * 2^(esig - 15) (|.| <
+// 2^14) against 2^15 on the row side. Zero-weight and padding columns carry
+// beta = +inf (fp16 +inf against 2^15: the score is +inf, never a minimum).
+//
+// Error bound per row i and stage t, in log2 units of q (u = 2^-24):
+//   * inputs rounded to fp32, then split in two tf32 parts: each factor is
+//     represented to 2^-22 relative, the lo.lo product is dropped: <= 14 u per
+//     product |a||b|;
+//   * values below fp16's normal range after scaling are off by <= 2^-25
+//     against a partner <= 2^14: 2^-11-esig per product, below 2^-38 of
+//     max|a| max|b| (or 2^-40 of max|beta|): covered by 2 u of the bound's
+//     magnitude term through kTcpFloor below;
+//   * the bias is exact to 2^-33 relative;
+//   * K' = 3 K + 3 products accumulate in fp32 inside the tensor core; with
+//     truncation instead of rounding every step loses <= 2 u of the running
+//     magnitude: 2 K' u.
+//   E_it = (2 K' + 32) u (1 + 2^-10) (Bb_t + |a_i|_2 |B_t|_2) + floor
+// with B_tk, Bb_t the stage's largest |b_jk| and finite |beta_j|
+// (Cauchy-Schwarz over k: one FMA per row and stage). tests/ check the bound
+// against the exact fp64 minima, and tools/f64s_probe_check.py prints the
+// largest observed error against it. The probe stores tmin = round_down(min_j
+// fl(q_ij) - E_it) and publishes slack = max 2 E_it, as the FFMA2 probe does.
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "softmin.cuh"
+#include "softmin_tc.cuh"
+
+namespace cntgw {
+
+template <int KX>
+struct TcpLayout {
+  static constexpr int kKp = (3 * KX + 3 + 15) / 16 * 16;  // halfs per row / column
+  static constexpr int kChunks = kKp / 8;                   // 16-byte K chunks
+  static constexpr int kMmas = kKp / 16;
+  static constexpr int kATileBytes = kChunks * kTcRows * 16;
+  static constexpr int kHH = 0, kLH = KX, kHL = 2 * KX, kBias = 3 * KX;
+  static constexpr int kP = kKp / 2;  // floats per column of the fp16 stage tiles
+};
+constexpr int kTcpStages = 3;  // shared-memory ring depth
+
+// Device header after the per-stage bounds: absmax words (float bits) of the
+// row features, column features and finite betas, then the scale exponents.
+struct TcpHeader {
+  uint32_t amax, bmax, betamax;
+  int esa, esb, esig;
+};
+
+// sbound region: [stages] float2 (|B_t|_2 rounded up, Bb_t) | TcpHeader
+__host__ __device__ inline size_t tcp_bounds_bytes(int stages) {
+  return align256(sizeof(float2) * (size_t)stages) + 256;
+}
+__device__ __forceinline__ TcpHeader* tcp_header(float* sbound, int stages) {
+  return reinterpret_cast<TcpHeader*>(reinterpret_cast<char*>(sbound) + align256(sizeof(float2) * (size_t)stages));
+}
+
+// (1 thread) a measuring sweep is about to probe: clear the absmax words
+__global__ void f64s_tcp_begin_kernel(float* sbound, int stages) {
+  TcpHeader* h = tcp_header(sbound, stages);
+  h->amax = h->bmax = h->betamax = 0u;
+}
+
+// one block per stage (gated on *full): the stage's bounds, the side's
+// absmax words, non-finite records
+template <int KX>
+__global__ void __launch_bounds__(128) f64s_tcp_stats_kernel(const int* full, const double* rec, int stride,
+                                                             int64_t m, int tile, float* sbound, int stages,
+                                                             int* nan) {
+  if (!*full) return;
+  __shared__ float red[4][KX + 1];
+  float bmax[KX + 1];
+#pragma unroll
+  for (int k = 0; k <= KX; ++k) bmax[k] = 0.f;
+  bool bad = false;
+  const int64_t j0 = (int64_t)blockIdx.x * tile;
+  for (int u = threadIdx.x; u < tile; u += blockDim.x) {
+    const int64_t j = j0 + u;
+    if (j >= m) continue;
+    const double* r = rec + j * stride;
+#pragma unroll
+    for (int k = 0; k < KX; ++k) {
+      const double v = r[k];
+      bad |= !(fabs(v) < 1e30);
+      bmax[k] = fmaxf(bmax[k], fabsf((float)v));
+    }
+    const double beta = r[KX];
+    bad |= (beta != beta) || beta == -CUDART_INF || (!(fabs(beta) < 1e30) && beta != CUDART_INF);
+    if (beta != CUDART_INF) bmax[KX] = fmaxf(bmax[KX], __double2float_ru(fabs(beta)));
+  }
+  if (bad) atomicOr(nan, 1);
+#pragma unroll
+  for (int k = 0; k <= KX; ++k) {
+    float v = bmax[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float n2 = 0.f, bm = 0.f;
+    for (int k = 0; k < KX; ++k) {
+      float v = red[0][k];
+      for (int w = 1; w < 4; ++w) v = fmaxf(v, red[w][k]);
+      n2 = __fmaf_ru(v, v, n2);
+      bm = fmaxf(bm, v);
+    }
+    float bb = red[0][KX];
+    for (int w = 1; w < 4; ++w) bb = fmaxf(bb, red[w][KX]);
+    reinterpret_cast<float2*>(sbound)[blockIdx.x] = make_float2(__fsqrt_ru(n2), bb);
+    TcpHeader* h = tcp_header(sbound, stages);
+    if (bm > 0.f) atomicMax(&h->bmax, __float_as_uint(bm));
+    if (bb > 0.f) atomicMax(&h->betamax, __float_as_uint(bb));
+  }
+}
+
+// grid-stride over the rows block (gated on *full): non-finite row features, absmax
+__global__ void f64s_tcp_rows_kernel(const int* full, const void* rows_block, int64_t n, int kd, int sq,
+                                     float* sbound, int stages, int* nan) {
+  if (!*full) return;
+  const char* rb = static_cast<const char*>(rows_block);
+  const double* rf = reinterpret_cast<const double*>(rb + align256(sizeof(int64_t) * n));
+  const double* rs = reinterpret_cast<const double*>(rb + align256(sizeof(int64_t) * n) +
+                                                     align256(sizeof(double) * n * kd));
+  bool bad = false;
+  float mx = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int k = 0; k < kd; ++k) {
+      const double v = rf[i * kd + k];
+      bad |= !(fabs(v) < 1e30);
+      mx = fmaxf(mx, fabsf((float)v));
+    }
+    if (sq) {
+      bad |= !(fabs(rs[i]) < 1e30);
+      mx = fmaxf(mx, fabsf((float)rs[i]));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx > 0.f && mx < CUDART_INF_F)
+    atomicMax(&tcp_header(sbound, stages)->amax, __float_as_uint(mx));
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nan, 1);
+}
+
+// (1 thread, after the gate) the scale exponents of this probe
+__global__ void f64s_tcp_scales_kernel(const int* probe_ok, float* sbound, int stages) {
+  if (!*probe_ok) return;
+  TcpHeader* h = tcp_header(sbound, stages);
+  auto ex = [](uint32_t bits) {  // 2^e > value (0 for an all-zero side)
+    const float v = __uint_as_float(bits);
+    return v > 0.f ? ilogbf(v) + 1 : 0;
+  };
+  const int ea = ex(h->amax), eb = ex(h->bmax), ebeta = ex(h->betamax);
+  int esig = 28 - ea - eb;
+  if (29 - ebeta < esig) esig = 29 - ebeta;
+  h->esa = 14 - ea;
+  h->esb = esig - (14 - ea);
+  h->esig = esig;
+}
+
+// one block per stage (gated on *probe_ok): the fp16 stage tile
+// [chunk][column][8 halfs] of the split column records
+template <int KX>
+__global__ void __launch_bounds__(128) f64s_tcp_pack_kernel(const int* probe_ok, const double* rec, int stride,
+                                                            int64_t m, int tile, __half* tiles, float* sbound,
+                                                            int stages) {
+  if (!*probe_ok) return;
+  using L = TcpLayout<KX>;
+  const TcpHeader* h = tcp_header(sbound, stages);
+  const float sb = pow2i(h->esb);
+  const double sbeta = exp2((double)(h->esig - 15));
+  __half* base0 = tiles + (int64_t)blockIdx.x * (L::kChunks * tile * 8);
+  const int64_t j0 = (int64_t)blockIdx.x * tile;
+  for (int u = threadIdx.x; u < tile; u += blockDim.x) {
+    const int64_t j = j0 + u;
+    __half* base = base0 + u * 8;
+    auto put = [&](int p, __half v) { base[(p >> 3) * (tile * 8) + (p & 7)] = v; };
+    for (int p = 0; p < L::kKp; ++p) put(p, __float2half_rn(0.f));
+    const double beta = j < m ? rec[j * stride + KX] : CUDART_INF;
+    if (j < m) {
+      const double* r = rec + j * stride;
+#pragma unroll
+      for (int k = 0; k < KX; ++k) {
+        const float b = (float)r[k];
+        const float bh = tf32_rna(b);
+        const float bl = tf32_rna(b - bh);
+        put(L::kHH + k, __float2half_rn(bh * sb));
+        put(L::kLH + k, __float2half_rn(bh * sb));
+        put(L::kHL + k, __float2half_rn(bl * sb));
+      }
+    }
+    if (beta == CUDART_INF) {
+      put(L::kBias, __ushort_as_half((unsigned short)0x7C00));  // +inf: no term
+    } else {
+      const double bs = beta * sbeta;
+      const __half b1 = __double2half(bs);
+      const double r1 = bs - (double)__half2float(b1);
+      const __half b2 = __double2half(r1);
+      const double r2 = r1 - (double)__half2float(b2);
+      put(L::kBias, b1);
+      put(L::kBias + 1, b2);
+      put(L::kBias + 2, __double2half(r2));
+    }
+  }
+}
+
+// The probe: one CTA = 128 ordered rows over one chunk of stages. Warp 0
+// streams the fp16 stage tiles (bulk copies into a 3-slot ring), warp 1 issues
+// the MMAs into NB = min(4, 512 / TD) TMEM accumulators of TD columns, and
+// 4 NB epilogue warps (TMEM lane quadrant q = warp % 4, accumulator p) take
+// the minimum of every NB-th stage.
+template <int KX, int TD>
+__global__ void __launch_bounds__(64 + 128 * (512 / TD < 4 ? 512 / TD : 4), 1)
+    f64s_tcp_kernel(const int* probe_ok, const void* rows_block, int64_t n, int kd, const __half* tiles,
+                    float* sbound, int stages, int chunk_stages, float* tmin, float* slack) {
+  using L = TcpLayout<KX>;
+  constexpr int NB = 512 / TD < 4 ? 512 / TD : 4;
+  constexpr int kBStageBytes = L::kChunks * TD * 16;
+  constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(TD >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
+  extern __shared__ __align__(1024) char smem_tcp[];
+  __shared__ uint64_t full_bar[kTcpStages], empty_bar[kTcpStages], tfull_bar[NB], tempty_bar[NB];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ float na_s[kTcRows];
+  if (!*probe_ok) return;
+
+  char* sA = smem_tcp;
+  char* sB = smem_tcp + L::kATileBytes;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = (int64_t)blockIdx.x * kTcRows;
+  const int t0 = blockIdx.y * chunk_stages;
+  const int nt = min(stages - t0, chunk_stages);
+  const TcpHeader* hdr = tcp_header(sbound, stages);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTcpStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < NB; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(&tmem_base_sh)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // A' rows: thread 64 + r packs row r (hi / lo parts scaled into fp16 range)
+  if (threadIdx.x >= 64 && threadIdx.x < 64 + kTcRows) {
+    const int r = threadIdx.x - 64;
+    const int64_t i = row0 + r;
+    const char* rb = static_cast<const char*>(rows_block);
+    const double* rf = reinterpret_cast<const double*>(rb + align256(sizeof(int64_t) * n));
+    const double* rs = reinterpret_cast<const double*>(rb + align256(sizeof(int64_t) * n) +
+                                                       align256(sizeof(double) * n * kd));
+    __half* hA = reinterpret_cast<__half*>(sA);
+    auto put = [&](int p, float v) { hA[(p >> 3) * (kTcRows * 8) + r * 8 + (p & 7)] = __float2half_rn(v); };
+    for (int p = 0; p < L::kKp; ++p) put(p, 0.f);
+    const float sa = pow2i(hdr->esa);
+    float n2 = 0.f;
+    for (int k = 0; k < KX; ++k) {
+      float a = 0.f;
+      if (i < n) a = (float)(k < kd ? rf[i * kd + k] : rs[i]);
+      const float ah = tf32_rna(a);
+      put(L::kHH + k, ah * sa);
+      put(L::kLH + k, tf32_rna(a - ah) * sa);
+      put(L::kHL + k, ah * sa);
+      n2 = __fmaf_ru(a, a, n2);
+    }
+    for (int p = 0; p < 3; ++p) put(L::kBias + p, 32768.f);
+    na_s[r] = __fsqrt_ru(n2);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> tensor-core proxy
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      const char* src = reinterpret_cast<const char*>(tiles) + (int64_t)t0 * kBStageBytes;
+      for (int t = 0, s = 0, ph = 0; t < nt; ++t) {
+        mbar_wait(&empty_bar[s], ph ^ 1);
+        mbar_expect_tx(&full_bar[s], kBStageBytes);
+        bulk_g2s(sB + s * kBStageBytes, src + (int64_t)t * kBStageBytes, kBStageBytes, &full_bar[s]);
+        if (++s == kTcpStages) s = 0, ph ^= 1;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      const uint32_t a0 = smem_u32(sA);
+      for (int t = 0, s = 0, ph = 0; t < nt; ++t) {
+        const int ab = t % NB;
+        mbar_wait(&full_bar[s], ph);
+        mbar_wait(&tempty_bar[ab], ((t / NB) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t b0 = smem_u32(sB + s * kBStageBytes);
+        const uint32_t d = tmem + (uint32_t)(ab * TD);
+#pragma unroll
+        for (int ks = 0; ks < L::kMmas; ++ks) {
+          const uint64_t ad = umma_desc(a0 + ks * 2 * (kTcRows * 16), kTcRows * 16, 128);
+          const uint64_t bd = umma_desc(b0 + ks * 2 * (TD * 16), TD * 16, 128);
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+              "l"(ad), "l"(bd), "r"(kIdesc), "r"(ks > 0 ? 1u : 0u));
+        }
+        tc_commit(&empty_bar[s]);
+        tc_commit(&tfull_bar[ab]);
+        if (++s == kTcpStages) s = 0, ph ^= 1;
+      }
+    }
+  } else {  // epilogue warps
+    const int q = warp & 3;            // TMEM lane quadrant (rows 32q..32q+31)
+    const int part = (warp - 2) >> 2;  // accumulator: stages part, part + NB, ...
+    const int r = 32 * q + lane;
+    const int64_t i = row0 + r;
+    const float na = na_s[r];
+    const float inv_sig = pow2i(-hdr->esig);
+    constexpr float kE = (float)(2 * L::kKp + 32) * 0x1p-24f * (1.f + 0x1p-10f);
+    // values flushed below fp16's normal range: 2^-25 against a partner <= 2^14 per product
+    // (2^15 for the bias parts), in accumulator units
+    const float floor_e = (float)(L::kKp + 4) * 0x1p-11f * inv_sig;
+    float smax = 0.f;
+    float va[32], vb[32];
+    for (int t = part; t < nt; t += NB) {
+      mbar_wait(&tfull_bar[part], (t / NB) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(part * TD);
+      float mn = CUDART_INF_F;
+      tmem_ld32(taddr, va);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < TD / 32; ++c) {
+        float(&cur)[32] = (c & 1) ? vb : va;
+        float(&nxt)[32] = (c & 1) ? va : vb;
+        if (c + 1 < TD / 32) {
+          tmem_ld32(taddr + 32 * (c + 1), nxt);
+        } else {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[part]);
+        }
+#pragma unroll
+        for (int u = 0; u < 32; u += 2) mn = fmin3f(mn, cur[u], cur[u + 1]);
+        if (c + 1 < TD / 32) tmem_wait_ld();
+      }
+      const float2 sb = __ldg(reinterpret_cast<const float2*>(sbound) + (t0 + t));
+      const float e = __fmaf_ru(__fmaf_ru(na, sb.x, sb.y), kE, floor_e);
+      smax = fmaxf(smax, e);
+      if (i < n) tmin[i * stages + t0 + t] = __fsub_rd(mn * inv_sig, e);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+    if (lane == 0 && smax > 0.f) atomicMax(reinterpret_cast<int*>(slack), __float_as_int(__fmul_ru(2.f, smax)));
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+}  // namespace cntgw

@@ -406,17 +406,21 @@ def test_f64s_measured_plan_matches_dense_loop(env, k, anneal, monkeypatch):
 
 
 @pytest.mark.parametrize("anneal", [None, 0.05], ids=["fixed", "annealed"])
-@pytest.mark.parametrize("k", [3, 4])
-def test_f64s_probe_matches_fp64_measurement(env, k, anneal, monkeypatch):
-    """CNTGW_F64S with the fp32 probe (softmin_f64s_probe.cuh: the dense
-    measurement of each loop's first sweep as fp32 stage minima minus a
-    rigorous error bound) against the fp64 measuring sweep
-    (CNTGW_F64S_PROBE=0): both plans skip only terms below 2^-64 of their
-    rows' maxima, so the loops agree to fp64 rounding; and both equal the
-    dense fp64 loop."""
+@pytest.mark.parametrize("k,kind", [(3, "tc"), (4, "tc"), (3, "ffma"), (4, "ffma"), (8, "tc"), (16, "tc"),
+                                    (32, "tc"), (64, "tc")])
+def test_f64s_probe_matches_fp64_measurement(env, k, kind, anneal, monkeypatch):
+    """CNTGW_F64S with a probe (the dense measurement of each loop's first
+    sweep as stage minima minus a rigorous error bound: the tcgen05 probe,
+    softmin_f64s_tcprobe.cuh, at every width, and the fp32 FFMA2 probe,
+    softmin_f64s_probe.cuh, up to kd + sq = 8) against the fp64 measuring
+    sweep (CNTGW_F64S_PROBE=0): every plan skips only terms below 2^-48 of
+    their rows' maxima, so the loops agree to fp64 rounding; and both equal
+    the dense fp64 loop. (A probe value above the true stage minimum would
+    drop needed stages and show up here.)"""
     P, engine, S, O, torch, dev = env
+    monkeypatch.setenv("CNTGW_F64S_PROBE_TC", "1" if kind == "tc" else "0")
     rng = np.random.default_rng(41 + k)
-    n, m = 1 << 14, 3 << 12
+    n, m = (1 << 14, 3 << 12) if k <= 4 else (1 << 12, 3 << 11)
     cx = rng.standard_normal((16, k)) * 2.0
     x = cx[rng.integers(0, 16, n)] + rng.standard_normal((n, k)) * 0.5
     z = cx[rng.integers(0, 16, m)] @ np.linalg.qr(rng.standard_normal((k, k)))[0] \

@@ -1,0 +1,11 @@
+# session 3: tcgen05 plan probe: probe tests (timeout-guarded), C4/C5 step times, traces
+timeout 600 python -m pytest tests/test_gpu_softmin.py -q -m gpu -p no:cacheprovider -x -k "f64s_probe" > gpurun_out/s3_12_tests.log 2>&1; echo "tests rc=$?"; tail -15 gpurun_out/s3_12_tests.log | cut -c1-300
+timeout 900 python -m pytest tests/test_gpu_softmin.py tests/test_gpu_fullsize.py tests/test_gpu_solver.py -q -m gpu -p no:cacheprovider -x -k "f64s or fullsize or full_size or solver" > gpurun_out/s3_12_tests2.log 2>&1; echo "tests2 rc=$?"; tail -5 gpurun_out/s3_12_tests2.log | cut -c1-300
+timeout 600 python tools/f64s_trace.py 1048576 1 10 c4 > gpurun_out/s3_12_trace_c4.log 2>&1; head -10 gpurun_out/s3_12_trace_c4.log
+timeout 600 python tools/f64s_trace.py 262144 1 10 c5 > gpurun_out/s3_12_trace_c5.log 2>&1; head -10 gpurun_out/s3_12_trace_c5.log
+timeout 900 python tools/solve_bench.py c4 1048576 10 > gpurun_out/s3_12_c4.log 2>&1
+timeout 600 python tools/solve_bench.py c5 262144 10 > gpurun_out/s3_12_c5.log 2>&1
+python -c "
+import json
+for f in ('gpurun_out/s3_12_c4.log','gpurun_out/s3_12_c5.log'):
+    d=json.loads(open(f).read().strip().splitlines()[-1]); print(d['config'], d['seconds'], d['step_seconds'], d['objectives'][-1])"
