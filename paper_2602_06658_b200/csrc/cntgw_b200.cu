@@ -143,7 +143,7 @@ KernelPick pick_f64s() {
     k.tcp_pack_fn = (void*)f64s_tcp_pack_kernel<KD + SQ>;
     k.tcp_threads = 64 + 128 * NB;
     k.tcp_stage_bytes = (size_t)TL::kChunks * TD * 16;
-    k.tcp_smem = (size_t)TL::kATileBytes + kTcpStages * k.tcp_stage_bytes;
+    k.tcp_smem = (size_t)TL::kATileBytes + tcp_ring<KD + SQ, TD>() * k.tcp_stage_bytes;
     if (TL::kP > k.probe_p) k.probe_p = TL::kP;
   }
   return k;
@@ -372,8 +372,10 @@ int f64s_vote(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl, 
   const double T = te ? atof(te) : (schedule ? 48.0 : 64.0);
   f64s_vote_kernel<<<(unsigned)l.row_tiles, 256, 0, s>>>(pl.flag, pl.gmin, pl.tstar, pl.range, n, l.stages,
                                                          k.cta_rows, T, pl.need, pl.counter, gate);
+  // kept fraction above which the sweep measures anew: with the tcgen05 probe a fresh plan costs
+  // ~0.1 dense sweeps (probe + exact sweep on its plan), so walking more than 12% does not pay
   const char* fe = getenv("CNTGW_F64S_REMEASURE");
-  const double frac = fe ? atof(fe) : 0.25;
+  const double frac = fe ? atof(fe) : (f64s_tcp_enabled(k) ? 0.12 : 0.25);
   f64s_decide_kernel<<<1, 1, 0, s>>>(st, pl.flag, pl.counter, pl.next_measure, l.row_tiles * (int64_t)l.stages,
                                      frac, schedule, gate, skip, pl.sched, pl.full,
                                      f64s_probe_enabled(k) ? 1 : 0);

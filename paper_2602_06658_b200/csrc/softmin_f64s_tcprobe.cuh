@@ -55,7 +55,19 @@ struct TcpLayout {
   static constexpr int kHH = 0, kLH = KX, kHL = 2 * KX, kBias = 3 * KX;
   static constexpr int kP = kKp / 2;  // floats per column of the fp16 stage tiles
 };
-constexpr int kTcpStages = 3;  // shared-memory ring depth
+// Shared-memory ring depth: a stage tile is small (8 KB at kd + sq = 4) and
+// one stage lasts a few hundred cycles, against ~1500 cycles for a bulk copy
+// to land from L2, so the ring holds as many stages as fit in 192 KB (at most
+// 16). Measured at C4 2^20: 70 ms per probe with a 3-deep ring (the epilogue
+// warps waiting on the MMA warp waiting on the copies), 54 ms with 16. Also
+// measured, and slower (70 ms): all 16 epilogue warps taking 64 columns of
+// every stage with a named barrier per quadrant to join the partial minima.
+template <int KX, int TD>
+constexpr int tcp_ring() {
+  constexpr int a = TcpLayout<KX>::kATileBytes, b = TcpLayout<KX>::kChunks * TD * 16;
+  constexpr int fit = (196608 - a) / b;
+  return fit > 16 ? 16 : (fit < 2 ? 2 : fit);
+}
 
 // Device header after the per-stage bounds: absmax words (float bits) of the
 // row features, column features and finite betas, then the scale exponents.
@@ -233,6 +245,7 @@ __global__ void __launch_bounds__(64 + 128 * (512 / TD < 4 ? 512 / TD : 4), 1)
   using L = TcpLayout<KX>;
   constexpr int NB = 512 / TD < 4 ? 512 / TD : 4;
   constexpr int kBStageBytes = L::kChunks * TD * 16;
+  constexpr int kTcpStages = tcp_ring<KX, TD>();
   constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(TD >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
   extern __shared__ __align__(1024) char smem_tcp[];
   __shared__ uint64_t full_bar[kTcpStages], empty_bar[kTcpStages], tfull_bar[NB], tempty_bar[NB];
@@ -346,7 +359,7 @@ __global__ void __launch_bounds__(64 + 128 * (512 / TD < 4 ? 512 / TD : 4), 1)
       mbar_wait(&tfull_bar[part], (t / NB) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(part * TD);
-      float mn = CUDART_INF_F;
+      float m4[4] = {CUDART_INF_F, CUDART_INF_F, CUDART_INF_F, CUDART_INF_F};  // independent chains
       tmem_ld32(taddr, va);
       tmem_wait_ld();
 #pragma unroll
@@ -361,9 +374,10 @@ __global__ void __launch_bounds__(64 + 128 * (512 / TD < 4 ? 512 / TD : 4), 1)
           if (lane == 0) mbar_arrive(&tempty_bar[part]);
         }
 #pragma unroll
-        for (int u = 0; u < 32; u += 2) mn = fmin3f(mn, cur[u], cur[u + 1]);
+        for (int u = 0; u < 32; u += 2) m4[(u >> 1) & 3] = fmin3f(m4[(u >> 1) & 3], cur[u], cur[u + 1]);
         if (c + 1 < TD / 32) tmem_wait_ld();
       }
+      const float mn = fminf(fminf(m4[0], m4[1]), fminf(m4[2], m4[3]));
       const float2 sb = __ldg(reinterpret_cast<const float2*>(sbound) + (t0 + t));
       const float e = __fmaf_ru(__fmaf_ru(na, sb.x, sb.y), kE, floor_e);
       smax = fmaxf(smax, e);
