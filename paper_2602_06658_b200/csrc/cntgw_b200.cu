@@ -128,6 +128,9 @@ KernelPick pick_f64s() {
   k.smem = (size_t)2 * TD * ColLayout<double, KD, SQ>::kStride * sizeof(double);
   k.rec_bytes = ColLayout<double, KD, SQ>::kStride * sizeof(double);
   k.f64s_tile = TD;
+  // the sweeps are sparse (the probe re-plans above 12% kept), so their records fit the L2
+  // without column chunks: half the CTAs and no partials to combine at C4 2^20
+  k.l2_chunk_mb = 1024;
   if constexpr (KD + SQ <= 8) {
     constexpr int R = KD + SQ <= 4 ? 16 : 8;
     k.probe_fn = (void*)f64s_probe_kernel<KD, SQ, R, TD>;
@@ -576,6 +579,10 @@ Plan plan_softmin(int64_t n, int64_t m, const KernelPick& k) {
     const int64_t tile_bytes = (int64_t)k.rec_bytes * kColTile;
     const int64_t tiles_fit = budget / tile_bytes > 0 ? budget / tile_bytes : 1;
     min_c = (tiles + tiles_fit - 1) / tiles_fit;
+  }
+  if (k.f64s_tile > 0) {  // the F64S kernel lists at most 4096 stages per chunk
+    const int64_t cap = (tiles * kColTile + 4096LL * k.f64s_tile - 1) / (4096LL * k.f64s_tile);
+    if (cap > min_c) min_c = cap;
   }
   int best_c = (int)min_c;
   double best_eff = -1.0;
