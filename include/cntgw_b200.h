@@ -194,20 +194,29 @@ int cntgw_prep_cols_ctr(const cntgw_sweep_state* st, int kd, int sq_flag, const 
 /* ---- K1/K2, CNTGW_F64S: fp64 (DMMA) on ordered rows/columns with a measured
  * block-sparse plan (softmin_f64s.cuh) — cold problems without low-dimensional
  * locality (C5). Rows are gathered once per operator into a block in a caller
- * order (a clustering of the points), columns are packed in their order; the
- * first sweep of a loop (or any sweep whose column records moved by more than
- * the plan's margin) runs densely and measures, per (row group, column
- * stage), whether any row holds a term within 2^-80 of its maximum; the
- * other sweeps walk only those stages. Outputs are in the caller's order;
- * the workspace (cntgw_softmin_workspace) holds the plan. */
+ * order (a clustering of the points), columns are packed in their order. The
+ * first sweep of a loop (or any sweep whose re-vote keeps more than 12% of
+ * the pairs) probes every row's minimum exponent over every column stage on
+ * the tensor cores (lower bounds, softmin_f64s_tcprobe.cuh; CNTGW_F64S_PROBE=0:
+ * a dense fp64 measuring sweep instead), the exact sweeps record exact
+ * minima for the stages they walk, and every sweep walks only the (row
+ * group, stage) pairs that can hold a term within 2^-48 of a row's maximum
+ * (CNTGW_CTR_SKIP_T overrides). Outputs are in the caller's order; the
+ * workspace (cntgw_softmin_workspace) holds the plan and must stay with one
+ * (rows, cols) operator for the length of a loop. */
 size_t cntgw_f64s_rows_bytes(int64_t n, int kd);
 int cntgw_prep_rows_f64s(int kd, int sq_flag, const double* feat, int64_t ld, const double* sq,
                          const int64_t* order, int64_t n, void* rows, void* stream);
 /* Diagnostics of the plan in an F64S workspace: out (3 int64, device) =
  * [needed (row group, stage) pairs, all pairs, flags of the last sweep: bit 0
- * measured with the fp64 kernel, bit 1 planned by the fp32 probe]. */
+ * measured with the fp64 kernel, bit 1 planned by a probe]. */
 int cntgw_f64s_plan_density(int kd, int sq_flag, int64_t n, int64_t m, const void* workspace, int64_t* out,
                             void* stream);
+/* Host-side query: out (3 int64, host) = [byte offset in the workspace of the
+ * plan's stage minima tmin, fp32 [n][stages] indexed by ordered row; stages;
+ * columns per stage]. After a probe sweep tmin holds the probe's lower
+ * bounds (tests/test_gpu_softmin.py checks them against exact fp64 minima). */
+int cntgw_f64s_plan_layout(int kd, int sq_flag, int64_t n, int64_t m, int64_t* out);
 /* out = (Gamma == 0 ? order_if_zero : order_otherwise), decided on the device
  * (graph-capturable): at Gamma = 0 the GW cost depends on the points only
  * through (s_i - t_j)^2 and the squared-coordinate order makes the plan a band. */

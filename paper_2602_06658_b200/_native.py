@@ -104,6 +104,7 @@ SIGNATURES = {
     "cntgw_select_order": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "cntgw_f64s_rows_bytes": (c_size_t, [c_i64, c_int]),
     "cntgw_f64s_plan_density": (c_int, [c_int, c_int, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "cntgw_f64s_plan_layout": (c_int, [c_int, c_int, c_i64, c_i64, c_vp]),
     "cntgw_prep_rows_f64s": (c_int, [c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "cntgw_prep_cols_f64s": (c_int, [c_vp, c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,
                                      c_vp, c_vp]),

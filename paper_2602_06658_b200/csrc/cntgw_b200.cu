@@ -115,12 +115,12 @@ struct KernelPick {
   size_t tcp_stage_bytes = 0;
 };
 
-// CNTGW_F64S: the DMMA kernel's tiling (same choices as pick<F64>) on ordered
-// rows and columns with a measured block-sparse plan (softmin_f64s.cuh).
-template <int KD, int SQ>
-KernelPick pick_f64s() {
-  constexpr int RG = KD >= 64 ? 2 : (KD >= 16 ? 4 : 2), NT = KD >= 16 ? 1 : 4;
-  constexpr int TD = KD >= 64 ? 64 : (KD >= 16 ? 128 : 256), MB = KD >= 16 ? 3 : 4;
+// CNTGW_F64S: the DMMA kernel's tiling on ordered rows and columns with a
+// measured block-sparse plan (softmin_f64s.cuh). RG groups of 8 rows per warp
+// (32 RG rows per CTA = the plan's row group), NT 8-column tiles per step, TD
+// columns per stage, MB CTAs per SM.
+template <int KD, int SQ, int RG, int NT, int TD, int MB>
+KernelPick f64s_variant() {
   KernelPick k;
   k.fn = (void*)softmin_f64s_kernel<KD, SQ, RG, NT, TD, MB>;
   k.rows = 1;
@@ -150,6 +150,18 @@ KernelPick pick_f64s() {
     if (TL::kP > k.probe_p) k.probe_p = TL::kP;
   }
   return k;
+}
+
+// Plan granularity, measured on the 10-step solves (tools/gpu/r2_s3_20.sh, r2_s3_21.sh): the
+// row group is the unit the plan keeps or skips, so smaller groups walk fewer pairs at a lower
+// DMMA reuse of each B fragment. kd < 16 (C4 2^20): 32-row groups 16.1 s, 64-row 17.2 s.
+// 16 <= kd < 64 (C5 2^18): 128-row groups 17.1 s, 64-row 13.4 s, 32-row 13.2 s. (The stage
+// width TD is shared with the plan consumers' kernels and stays.)
+template <int KD, int SQ>
+KernelPick pick_f64s() {
+  constexpr int RG = KD >= 16 ? 2 : 1, NT = KD >= 16 ? 1 : 4;
+  constexpr int TD = KD >= 64 ? 64 : (KD >= 16 ? 128 : 256), MB = KD >= 64 ? 3 : (KD >= 16 ? 4 : 5);
+  return f64s_variant<KD, SQ, RG, NT, TD, MB>();
 }
 
 template <int PREC, int KD, int SQ>
@@ -1104,6 +1116,18 @@ int cntgw_f64s_plan_density(int kd, int sq_flag, int64_t n, int64_t m, const voi
   f64s_density_kernel<<<148, 256, 0, s>>>(pl.need, fl.row_tiles * (int64_t)fl.stages, pl.flag,
                                           f64s_probe_enabled(k) ? pl.probe_ok : nullptr, out);
   return check_launch("f64s_density");
+}
+
+/* Where the measured plan's stage minima live in an F64S workspace (host-side query). */
+int cntgw_f64s_plan_layout(int kd, int sq_flag, int64_t n, int64_t m, int64_t* out) {
+  KernelPick k;
+  if (!out || n < 1 || m < 1 || !lookup(CNTGW_F64S, kd, sq_flag, &k))
+    return fail(CNTGW_EINVAL, "f64s_plan_layout: bad arguments");
+  const F64sPlanLayout fl = f64s_layout(k, n, m);
+  out[0] = (int64_t)align256(plan_workspace(plan_softmin(n, m, k), n));  // tmin: [n][stages] fp32
+  out[1] = fl.stages;
+  out[2] = k.f64s_tile;
+  return CNTGW_OK;
 }
 
 /* ---- CNTGW_F64S: the point order of the next loop from the device Gamma ---- */

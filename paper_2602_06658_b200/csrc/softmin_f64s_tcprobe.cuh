@@ -23,19 +23,19 @@
 //     represented to 2^-22 relative, the lo.lo product is dropped: <= 14 u per
 //     product |a||b|;
 //   * values below fp16's normal range after scaling are off by <= 2^-25
-//     against a partner <= 2^14: 2^-11-esig per product, below 2^-38 of
-//     max|a| max|b| (or 2^-40 of max|beta|): covered by 2 u of the bound's
-//     magnitude term through kTcpFloor below;
+//     against a partner <= 2^14: 2^(-11-esig) per product, below 2^-38 of
+//     max|a| max|b| (or 2^-40 of max|beta|): the term floor_e of the kernel;
 //   * the bias is exact to 2^-33 relative;
 //   * K' = 3 K + 3 products accumulate in fp32 inside the tensor core; with
 //     truncation instead of rounding every step loses <= 2 u of the running
 //     magnitude: 2 K' u.
 //   E_it = (2 K' + 32) u (1 + 2^-10) (Bb_t + |a_i|_2 |B_t|_2) + floor
 // with B_tk, Bb_t the stage's largest |b_jk| and finite |beta_j|
-// (Cauchy-Schwarz over k: one FMA per row and stage). tests/ check the bound
-// against the exact fp64 minima, and tools/f64s_probe_check.py prints the
-// largest observed error against it. The probe stores tmin = round_down(min_j
-// fl(q_ij) - E_it) and publishes slack = max 2 E_it, as the FFMA2 probe does.
+// (Cauchy-Schwarz over k: one FMA per row and stage).
+// tests/test_gpu_softmin.py::test_f64s_probe_bounds checks the stored values
+// against exact fp64 stage minima at widths 3..64. The probe stores tmin =
+// round_down(min_j fl(q_ij) - E_it) and publishes slack = max 2 E_it, as the
+// FFMA2 probe does.
 #pragma once
 
 #include <cuda_fp16.h>

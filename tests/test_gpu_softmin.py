@@ -405,6 +405,65 @@ def test_f64s_measured_plan_matches_dense_loop(env, k, anneal, monkeypatch):
     assert _rel(got[rows], want) < 5e-7
 
 
+@pytest.mark.parametrize("k,kind", [(3, "tc"), (3, "ffma"), (8, "tc"), (32, "tc"), (64, "tc")])
+@pytest.mark.parametrize("zero_w", [False, True])
+def test_f64s_probe_bounds(env, k, kind, zero_w, monkeypatch):
+    """The probes store LOWER bounds of every row's minimum exponent q_ij =
+    beta_j + sum_k a_ik b_jk over every column stage, a few log2 units (the
+    published error bound) below the exact minima: read back from the plan
+    workspace after a first sweep and compared with minima recomputed in
+    fp64 from the device's own row block and column records."""
+    P, engine, S, O, torch, dev = env
+    from paper_2602_06658_b200._native import LIB
+
+    monkeypatch.setenv("CNTGW_F64S_PROBE_TC", "1" if kind == "tc" else "0")
+    monkeypatch.setenv("CNTGW_F64S_REMEASURE", "2.0")  # the exact sweep must not overwrite tmin
+    rng = np.random.default_rng(7 + k)
+    n, m = 1500, 2900
+    cx = rng.standard_normal((16, k)) * (2.0 if k <= 8 else 0.5)
+    x = cx[rng.integers(0, 16, n)] + rng.standard_normal((n, k)) * 0.5
+    z = cx[rng.integers(0, 16, m)] + rng.standard_normal((m, k)) * 0.5
+    a = np.full(n, 1 / n)
+    b = np.where(np.arange(m) % 5 == 2, 0.0, 1.0) if zero_w else np.ones(m)
+    b /= b.sum()
+    g = rng.standard_normal(m) * 3.0 + (z * z).sum(1)
+    eps = 2.5e-3
+    prob = S.device_problem(P.SquaredEuclideanCost(x, z), a, b, dev)
+    op = prob.fwd
+    op.prec = 4
+    st = engine.SweepState(dev)
+    st.init(eps)
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    op(st, engine.to_dev64(g - prob.col_sep, dev), out, skip=False)
+    torch.cuda.synchronize()
+    lay = np.zeros(3, dtype=np.int64)
+    assert LIB.cntgw_f64s_plan_layout(op.kd, 1, n, m, lay.ctypes.data) == 0
+    off, stages, td = (int(v) for v in lay)
+    tmin = op.ws[off:off + 4 * n * stages].view(torch.float32).reshape(n, stages).cpu().numpy().astype(np.float64)
+    kd = op.kd
+    stride = LIB.cntgw_col_stride(4, kd, 1)
+    mpad = stages * td
+    rec = op.rec[:mpad * stride].reshape(mpad, stride).cpu().numpy()
+    rows = op.f64s_rows.cpu().numpy()
+    a256 = lambda v: (v + 255) // 256 * 256
+    feat = rows[a256(8 * n):a256(8 * n) + 8 * n * kd].view(np.float64).reshape(n, kd)
+    sq = rows[a256(8 * n) + a256(8 * n * kd):a256(8 * n) + a256(8 * n * kd) + 8 * n].view(np.float64)
+    arow = np.concatenate([feat, sq[:, None]], axis=1)
+    q = arow @ rec[:, :kd + 1].T + rec[None, :, kd + 1]
+    q[:, m:] = np.inf  # padding columns
+    exact = q.reshape(n, stages, td).min(axis=2)
+    finite = np.isfinite(exact)
+    assert np.all(np.isinf(tmin[~finite]) & (tmin[~finite] > 0))
+    gap = exact[finite] - tmin[finite]
+    assert gap.min() >= 0.0, f"probe value above the exact stage minimum by {-gap.min():.3e}"
+    # ... and not uselessly loose: within a few units of the bound's own size
+    scale = np.abs(rec[:m, kd + 1]).max() + np.linalg.norm(arow, axis=1).max() * np.linalg.norm(
+        np.abs(rec[:m, :kd + 1]).max(axis=0))
+    kp = (3 * (kd + 1) + 3 + 15) // 16 * 16
+    bound = ((2 * kp + 32) if kind == "tc" else (kd + 5)) * 2.0 ** -24 * scale
+    assert gap.max() <= 2.5 * bound + 1e-3, (gap.max(), bound)
+
+
 @pytest.mark.parametrize("anneal", [None, 0.05], ids=["fixed", "annealed"])
 @pytest.mark.parametrize("k,kind", [(3, "tc"), (4, "tc"), (3, "ffma"), (4, "ffma"), (8, "tc"), (16, "tc"),
                                     (32, "tc"), (64, "tc")])
