@@ -160,7 +160,7 @@ KernelPick f64s_variant() {
 template <int KD, int SQ>
 KernelPick pick_f64s() {
   constexpr int RG = KD >= 16 ? 2 : 1, NT = KD >= 16 ? 1 : 4;
-  constexpr int TD = KD >= 64 ? 64 : (KD >= 16 ? 128 : 256), MB = KD >= 64 ? 3 : (KD >= 16 ? 4 : 5);
+  constexpr int TD = f64s_stage_cols(KD), MB = KD >= 64 ? 3 : (KD >= 16 ? 4 : 5);
   return f64s_variant<KD, SQ, RG, NT, TD, MB>();
 }
 
@@ -1314,7 +1314,7 @@ int cntgw_plan_reduce_f64s(const cntgw_sweep_state* st, int kd, int sq_flag, int
 #define PRS(KD_, E_)                                                                                 \
   if (kd == KD_ && ep == E_) {                                                                       \
     constexpr int KX = KD_ + 1, STR = ColLayout<double, KD_, 1>::kStride;                           \
-    constexpr int TD = KD_ >= 64 ? 64 : (KD_ >= 16 ? 128 : 256);                                     \
+    constexpr int TD = f64s_stage_cols(KD_);                                                         \
     auto kern = plan_reduce_ctr_kernel<KX, E_, 4, STR, TD>;                                          \
     const size_t smem = CtrReduceSmem<STR, E_, TD>::kBytes;                                          \
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \

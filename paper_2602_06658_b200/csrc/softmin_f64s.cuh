@@ -35,6 +35,10 @@
 
 namespace cntgw {
 
+// Columns per stage of the measured plan, shared by the sweeps, the probes and
+// the plan consumers (K4): the unit of columns the plan keeps or skips.
+constexpr int f64s_stage_cols(int kd) { return kd >= 16 ? 64 : 256; }
+
 struct F64sArgs {
   const int64_t* row_order;  // ordered position -> caller row (rows block)
   const int* replan;         // this sweep measures (writes tmin for the stages it walks)
