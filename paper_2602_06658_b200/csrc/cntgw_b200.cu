@@ -152,15 +152,16 @@ KernelPick f64s_variant() {
   return k;
 }
 
-// Plan granularity, measured on the 10-step solves (tools/gpu/r2_s3_20.sh, r2_s3_21.sh): the
-// row group is the unit the plan keeps or skips, so smaller groups walk fewer pairs at a lower
-// DMMA reuse of each B fragment. kd < 16 (C4 2^20): 32-row groups 16.1 s, 64-row 17.2 s.
-// 16 <= kd < 64 (C5 2^18): 128-row groups 17.1 s, 64-row 13.4 s, 32-row 13.2 s. (The stage
-// width TD is shared with the plan consumers' kernels and stays.)
+// Plan granularity, measured on the 10-step solves (tools/gpu/r2_s3_20.sh .. r2_s3_25.sh): the
+// (row group, column stage) block is the unit the plan keeps or skips, so smaller blocks walk
+// fewer pairs at a lower DMMA reuse of each B fragment and a longer probe (more stages).
+// kd < 16 (C4 2^20): 32-row groups 16.1 s, 64-row 17.2 s; 128-column stages 18.0 s (probe 67 ->
+// 109 ms). 16 <= kd < 64 (C5 2^18): 128 rows x 128 columns 17.1 s, 64 x 128 13.3 s, 64 x 64
+// 11.2 s, 32 x 64 10.0 s. (The stage width is f64s_stage_cols, shared with the plan consumers.)
 template <int KD, int SQ>
 KernelPick pick_f64s() {
-  constexpr int RG = KD >= 16 ? 2 : 1, NT = KD >= 16 ? 1 : 4;
-  constexpr int TD = f64s_stage_cols(KD), MB = KD >= 64 ? 3 : (KD >= 16 ? 4 : 5);
+  constexpr int RG = KD >= 64 ? 2 : 1, NT = KD >= 16 ? 1 : 4;
+  constexpr int TD = f64s_stage_cols(KD), MB = KD >= 64 ? 3 : 5;
   return f64s_variant<KD, SQ, RG, NT, TD, MB>();
 }
 
