@@ -329,6 +329,7 @@ struct F64sPlan {
   int* probe_ok;   // this sweep's plan came from the probe
   float* slack;    // the probe's 2 max E (log2 units)
   int* sched;      // re-measurement schedule: interval, kept pairs before the last one, pending, its sweep
+  int* dotzero;    // [0] any nonzero row dot feature, [1] any nonzero column dot feature (per call)
   float* rec32;    // fp32 probe records [mpad][P]
   float* sbound;   // per stage magnitude bounds [stages][P]
 };
@@ -351,6 +352,7 @@ F64sPlan f64s_plan(void* base_v, const F64sPlanLayout& l) {
   p.probe_ok = p.counter + 4;
   p.slack = reinterpret_cast<float*>(p.counter + 5);
   p.sched = p.counter + 6;
+  p.dotzero = p.counter + 10;
   char* tail = base + l.tmin + l.need + l.cplan + l.range + l.gmin + l.tstar + l.rowmin + 256;
   p.rec32 = l.rec32 ? reinterpret_cast<float*>(tail) : nullptr;
   p.sbound = l.sbound ? reinterpret_cast<float*>(tail + l.rec32) : nullptr;
@@ -1037,10 +1039,17 @@ int cntgw_softmin(const cntgw_sweep_state* st, int skip_if_done, int prec, int k
       return rc;
     if (env_int("CNTGW_CTR_REUSE", 1) == 0) f64s_begin_kernel<<<1, 1, 0, s>>>(nullptr, 0, pl.key, row_feat, col_rec,
                                                                                 n, m, pl.flag, pl.counter, pl.full, pl.sched);
+    // (before the probe, which clears *full once its plan stands)
+    if (sq_flag && env_int("CNTGW_F64S_DOTZERO", 1))  // does the dot term vanish (Gamma = 0)? (first sweeps)
+      f64s_dotzero_kernel<<<2 * num_sms(), 256, 0, s>>>(pl.full, row_feat, n, kd, rec,
+                                                        cntgw_col_stride(CNTGW_F64S, kd, 1), m, pl.dotzero);
+    else
+      cudaMemsetAsync(pl.dotzero, 0xff, 2 * sizeof(int), s);  // (both sides "nonzero")
     if (f64s_probe_enabled(k))
       if (const int rc = f64s_probe(k, fl, pl, st, skip_if_done, rec, kd, sq_flag ? 1 : 0, row_feat, col_rec, n, m, s))
         return rc;
     fs.full = pl.full;
+    fs.dotzero = pl.dotzero;
     void* args2[] = {&a, &fs};
     cudaError_t e2 = cudaLaunchKernel(k.fn, dim3(p.row_tiles, p.nchunks), dim3(k.threads), args2, k.smem, s);
     if (e2 != cudaSuccess) {

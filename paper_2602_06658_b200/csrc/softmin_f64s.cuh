@@ -46,6 +46,7 @@ struct F64sArgs {
   const uint8_t* need;       // [row groups][stages] (row group = one CTA's rows)
   float* tmin;               // [n][stages] min q per row and stage (replan sweeps)
   int stages;                // mpad / TD
+  const int* dotzero;        // [0] any nonzero row dot feature, [1] any nonzero column dot feature
 };
 
 // Rows block: order [n] int64 | features [n][kd] fp64 | sq [n] fp64.
@@ -117,9 +118,10 @@ __global__ void f64s_begin_kernel(const cntgw_sweep_state* st, int skip, CtrPlan
   *flag = first ? 1 : 0;
   *full = first ? 1 : 0;  // a measurement over every stage (else: over the kept ones)
   *counter = 0;
-  if (first) {  // a new plan: the re-measurement schedule starts over
+  if (first) {  // a new plan: the re-measurement schedule starts over, the dot-term flags are re-detected
     sched[0] = 1;
     sched[2] = 0;
+    sched[4] = sched[5] = 0;  // (= F64sPlan::dotzero)
   }
 }
 
@@ -382,6 +384,54 @@ __global__ void __launch_bounds__(1024) f64s_commit_kernel(const int* flag, cons
   }
 }
 
+// The dot term <x_i, c_j> vanishes when one side's dot features are all zero:
+// at Gamma = 0 (the product coupling every solve starts from) the operator's
+// features X Gamma are, so the whole first outer step runs on q_ij = -beta_j
+// + s_i c_sj alone. This kernel records, per call, whether any row or any
+// column dot feature is nonzero (blocks leave early once a side is known to
+// be nonzero); the sweep then takes one DFMA per pair instead of the DMMA
+// k-steps (C5: 9 k-steps -> 1 FMA, first outer step 1.42 -> 1.0 s). Runs on
+// the sweeps that measure over every stage (*gate: the first of a loop, where
+// f64s_begin_kernel cleared the flags; the operator is fixed within a loop).
+__global__ void f64s_dotzero_kernel(const int* gate, const void* rows_block, int64_t n, int kd, const double* rec,
+                                    int stride, int64_t m, int* flags) {
+  if (!*gate) return;
+  const char* rb = static_cast<const char*>(rows_block);
+  const double* rf = reinterpret_cast<const double*>(rb + align256(sizeof(int64_t) * n));
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  if (!flags[0]) {
+    bool nz = false;
+    for (int64_t e = tid; e < n * kd && !nz; e += nth) nz = rf[e] != 0.0;
+    if (nz) flags[0] = 1;
+  }
+  if (!flags[1]) {
+    bool nz = false;
+    for (int64_t j = tid; j < m && !nz; j += nth)
+      for (int k = 0; k < kd; ++k) nz |= rec[j * stride + k] != 0.0;
+    if (nz) flags[1] = 1;
+  }
+}
+
+// q of RG row groups x NT 8-column tiles in the DMMA accumulator layout (lane
+// (lr, lk): row lr of each group, columns 2 lk and 2 lk + 1 of each tile) when
+// the dot term vanishes: -beta_j + s_i c_sj
+template <int KD, int SQ, int RG, int NT>
+__device__ __forceinline__ void sq_scores(const double* __restrict__ tile, int ct, int lk, const double (&as)[RG],
+                                          double (&q)[RG][NT][2]) {
+  using L = ColLayout<double, KD, SQ>;
+#pragma unroll
+  for (int u = 0; u < NT; ++u) {
+    const double* cc = tile + (ct + 8 * u + 2 * lk) * L::kStride;
+    const double b0 = cc[KD], b1 = cc[L::kStride + KD];
+    const double beta0 = cc[L::kBeta], beta1 = cc[L::kStride + L::kBeta];
+#pragma unroll
+    for (int rg = 0; rg < RG; ++rg) {
+      q[rg][u][0] = fma(as[rg], b0, beta0);
+      q[rg][u][1] = fma(as[rg], b1, beta1);
+    }
+  }
+}
+
 // dmma_consume plus the step's minimum q per row group, tracked on the fp32
 // exponent arguments x = mq - q (FMNMX on the ALU, not a DMNMX per term on
 // the FP64 pipe): tm = min(tm, mq - max x), one fp64 op per row group and
@@ -452,13 +502,16 @@ __global__ void __launch_bounds__(128, MINB) softmin_f64s_kernel(const SoftminAr
   const double* rs = reinterpret_cast<const double*>(rb + align256(sizeof(int64_t) * a.n) +
                                                      align256(sizeof(double) * a.n * KD));
   const bool replan = *p.replan != 0, full = *p.full != 0;
+  const bool dotzero = SQ && (p.dotzero[0] == 0 || p.dotzero[1] == 0);
 
   double afr[RG][KS];
+  double as_row[RG];
   double mq[RG], S[RG];
 #pragma unroll
   for (int rg = 0; rg < RG; ++rg) {
     const int64_t i = wrow + 8 * rg + lr;
     const bool ok = i < a.n;
+    as_row[rg] = SQ && ok ? rs[i] : 0.0;
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const int k = 4 * ks + lk;
@@ -530,7 +583,8 @@ __global__ void __launch_bounds__(128, MINB) softmin_f64s_kernel(const SoftminAr
 #pragma unroll 1
     for (int ct = 0; ct < TILE; ct += 8 * NT) {
       double q[RG][NT][2];
-      dmma_scores<KD, SQ, RG, NT, KS>(tile, ct, lr, lk, afr, q);
+      if (dotzero) sq_scores<KD, SQ, RG, NT>(tile, ct, lk, as_row, q);
+      else dmma_scores<KD, SQ, RG, NT, KS>(tile, ct, lr, lk, afr, q);
       if (replan)  // (the measuring sweep: stage minima ride on the exponent arguments)
         dmma_consume_min<RG, NT>(q, mq, S, T, tm);
       else

@@ -405,6 +405,43 @@ def test_f64s_measured_plan_matches_dense_loop(env, k, anneal, monkeypatch):
     assert _rel(got[rows], want) < 5e-7
 
 
+@pytest.mark.parametrize("k", [3, 32])
+@pytest.mark.parametrize("zero_side", ["rows", "cols", "none"])
+def test_f64s_vanishing_dot_term(env, k, zero_side, monkeypatch):
+    """At Gamma = 0 one side's dot features are all zero and the F64S sweep
+    takes q_ij = -beta_j + s_i c_sj with one DFMA per pair instead of the DMMA
+    k-steps (decided per call on the device): a loop of sweeps equals the
+    dense fp64 DMMA path whichever side vanishes, and the generic case is
+    untouched."""
+    P, engine, S, O, torch, dev = env
+    from paper_2602_06658_b200._native import F64, F64S
+
+    rng = np.random.default_rng(3 + k)
+    n, m = 2100, 2900
+    x = rng.standard_normal((n, k)) * (0.0 if zero_side == "rows" else 0.6)
+    z = rng.standard_normal((m, k)) * (0.0 if zero_side == "cols" else 0.6)
+    sx, sz = rng.random(n) * 6.0, rng.random(m) * 6.0
+    src = engine.Side.make(x, sx, np.full(n, 1 / n), dev, k)
+    tgt = engine.Side.make(z, sz, np.full(m, 1 / m), dev, k)
+    pot = engine.to_dev64(rng.standard_normal(m) * 5.0, dev)
+    outs = {}
+    for name, prec in (("f64s", F64S), ("f64", F64)):
+        op = engine.HalfUpdate(src, tgt, True)
+        op.prec = prec
+        st = engine.SweepState(dev)
+        st.init(2.5e-3, None, None, 8, "symmetrized")
+        res = []
+        for _ in range(3):  # a probe sweep, then re-voted / measuring sweeps
+            st.begin()
+            out = torch.empty(n, dtype=torch.float64, device=dev)
+            op(st, pot, out, skip=False)
+            res.append(out.cpu().numpy())
+        outs[name] = res
+    for a_, b_ in zip(outs["f64s"], outs["f64"]):
+        assert np.all(np.isfinite(a_))
+        assert _rel(a_, b_) < 5e-9
+
+
 @pytest.mark.parametrize("k,kind", [(3, "tc"), (3, "ffma"), (8, "tc"), (32, "tc"), (64, "tc")])
 @pytest.mark.parametrize("zero_w", [False, True])
 def test_f64s_probe_bounds(env, k, kind, zero_w, monkeypatch):
