@@ -354,7 +354,7 @@ class HalfUpdate:
         self.rows, self.cols, self.sq = rows, cols, bool(sq)
         self.kd = rows.kd
         assert cols.kd == self.kd
-        self.prec = prec
+        self._prec = F32
         dev = rows.feat64.device
         precs = (F32, F64, TF32X3) if tc_supported(self.kd, self.sq) else (F32, F64)
         rec_bytes = 0
@@ -374,6 +374,10 @@ class HalfUpdate:
         wsb = max(LIB.cntgw_softmin_workspace(p, rows.n, cols.n, self.kd, int(self.sq)) for p in precs)
         self.ws = torch.empty(max(int(wsb), 16), dtype=torch.uint8, device=dev)
         self.f64s_rows = None
+        # CNTGW_F64S: the rows block (order | features | s) is fixed within a loop; a driver that
+        # owns the loop gathers it once (hoist_rows) instead of once per half-update
+        self.rows_hoisted = False
+        self.prec = prec  # (the setter sizes the F64S buffers: after the fields above)
 
     @property
     def prec(self) -> int:
@@ -421,8 +425,8 @@ class HalfUpdate:
             feat, rec = self.ctr_rows, self.ctr_cols
         elif self.prec == F64S:
             sq = r.sq64 if self.sq else None
-            call("cntgw_prep_rows_f64s", self.kd, int(self.sq), r.feat64.data_ptr(), self.kd, _p(sq),
-                 r.plan_order().data_ptr(), r.n, self.f64s_rows.data_ptr(), _stream())
+            if not self.rows_hoisted:
+                self._prep_rows_f64s()
             feat, rec = self.f64s_rows, self.rec
         else:
             feat, sq = r.feat(self.prec)
@@ -430,6 +434,20 @@ class HalfUpdate:
         call("cntgw_softmin", state.ptr, int(skip), self.prec, self.kd, int(self.sq),
              feat.data_ptr(), self.kd, _p(sq), _p(row_add), rec.data_ptr(), r.n, self.cols.n,
              _p(out), _p(out_max), _p(out_sum), self.ws.data_ptr(), self.ws.numel(), _stream())
+
+    def _prep_rows_f64s(self):
+        r = self.rows
+        call("cntgw_prep_rows_f64s", self.kd, int(self.sq), r.feat64.data_ptr(), self.kd,
+             _p(r.sq64 if self.sq else None), r.plan_order().data_ptr(), r.n, self.f64s_rows.data_ptr(),
+             _stream())
+
+    def hoist_rows(self):
+        """Gather the F64S rows block now and skip the per-call gather until
+        ``rows_hoisted`` is cleared (the owner clears it whenever the row
+        features or their order change)."""
+        if self.prec == F64S:
+            self._prep_rows_f64s()
+            self.rows_hoisted = True
 
     def __call__(self, state, pot_cols, out, skip=True, row_add=None):
         self.pack(state, pot_cols)
@@ -509,6 +527,18 @@ class SinkhornLoop:
         for op in (self.fwd, self.bwd):
             if isinstance(op, HalfUpdate):
                 op.prec = prec
+                op.rows_hoisted = False
+
+    def hoist_rows(self):
+        """Once per loop (fixed features, order and path): see HalfUpdate.hoist_rows."""
+        for op in (self.fwd, self.bwd):
+            if isinstance(op, HalfUpdate):
+                op.hoist_rows()
+
+    def unhoist_rows(self):
+        for op in (self.fwd, self.bwd):
+            if isinstance(op, HalfUpdate):
+                op.rows_hoisted = False
 
     # -- one sweep (every launch is a no-op once the state says done) --------
     def _g_update(self, f, out, skip=True):

@@ -274,6 +274,7 @@ class _GwDevice:
         self._select_orders(g)
 
     def _select_orders(self, gamma_dev: torch.Tensor):
+        self.loop.unhoist_rows()  # new features (and maybe a new order): the rows blocks are stale
         for sq_order, geo, cur in self._orders:
             call("cntgw_select_order", gamma_dev.data_ptr(), self.d * self.e, sq_order.data_ptr(),
                  geo.data_ptr(), cur.numel(), cur.data_ptr(), _stream())
@@ -426,6 +427,7 @@ class _GwDevice:
              const: float, use_graph: bool):
         self.set_gamma(gamma)
         self.choose_precision(f, g, loop_cfg.eps)
+        self.loop.hoist_rows()
         stats = self.loop.run(f, g, loop_cfg, use_graph=use_graph)
         # g-tentative (skipped on the device after a symmetrized threshold
         # break, whose tentatives are already the final ones), K4, K7
@@ -604,6 +606,7 @@ class _DeviceSolve:
             call("cntgw_graph_while_begin", s0.cuda_stream, s1.cuda_stream, ctypes.byref(h1))
             with torch.cuda.stream(s1):
                 dev.set_gamma_dev(self.gamma, self.gamma_t)
+                loop.hoist_rows()
                 loop.state.init(lc.eps, lc.anneal_from, lc.threshold, lc.max_sweeps, lc.mode)
                 if lc.threshold is None:
                     for _ in range(lc.max_sweeps):
