@@ -508,7 +508,7 @@ def gw_solve_block(args, info, dev):
     out["c1"] = {"config": "C1 (N=M=1000, eps=0.01, tau=1e-5, <=20 outer)",
                  "seconds": max_ranks(e0.elapsed_time(e1) * 1e-3), "outer": len(res.trace),
                  "inner_iters": list(res.trace.inner_iters), "value": res.value}
-    paths = {0: "fp32", 1: "fp64 DMMA", 2: "tcgen05 3xTF32", 3: "block-sparse centred fp32 (F32C)",
+    paths = {0: "fp32", 1: "fp64 DMMA", 2: "tcgen05 split precision (fp16 operands)", 3: "block-sparse centred fp32 (F32C)",
              4: "fp64 DMMA + measured block-sparse plan (F64S)"}
 
     def stepped(key, pc, eps, inner, outer, label):

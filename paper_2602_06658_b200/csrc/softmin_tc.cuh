@@ -2,30 +2,36 @@
 // problems with K >= 8 dot features (the C2 micro-benchmark shape).
 //
 // t_ij = beta_j + sum_k x_ik (2 lam z_jk) is a GEMM-shaped score, evaluated as
-// a split-precision ("3xTF32") tcgen05 MMA so that it keeps ~fp32 accuracy:
-//     A'_i = [hi(x_i), 1 | hi(x_i), 1 | lo(x_i), 0]      (K' = 3 KD + 2, padded to 8)
-//     B'_j = [hi(zt_j), hi(b_j) | lo(zt_j), lo(b_j) | hi(zt_j), 0]
-//     A'_i . B'_j = hi.hi + hi.lo + lo.hi  (+ the bias, split exactly)
-// with hi = tf32 rounding and lo = tf32(x - hi). The accumulator lives in
-// TMEM (128 lanes = rows x 256 fp32 columns, double-buffered = all 512 TMEM
-// columns), so the FMA pipe does only the online log-sum-exp epilogue:
-// tcgen05.ld -> subtract the lazily rebased row reference -> MUFU.EX2 -> sum.
+// a split-precision tcgen05 MMA so that it keeps ~fp32 accuracy: with hi =
+// tf32 rounding and lo = tf32(x - hi),
+//     A'_i . B'_j = hi.hi + hi.lo + lo.hi  (+ the bias, split exactly).
+// Two operand formats (CNTGW_TC_KIND):
+//   * fp16 (default, TcLayoutH below): the 11-bit parts scaled into fp16's
+//     range, kind::f16 at K = 16 per instruction: 4 MMAs and 32 KB of B' per
+//     256 columns at KD = 16;
+//   * tf32 (TcLayout): A'_i = [hi(x_i), 1 | hi(x_i), 1 | lo(x_i), 0],
+//     B'_j = [hi(zt_j), hi(b_j) | lo(zt_j), lo(b_j) | hi(zt_j), 0], K' = 3 KD + 2
+//     padded to 8, kind::tf32 at K = 8: 7 MMAs and 56 KB.
+// The accumulator lives in TMEM (128 lanes = rows x 256 fp32 columns,
+// double-buffered = all 512 TMEM columns), so the FMA pipe does only the
+// online log-sum-exp epilogue: tcgen05.ld -> subtract the lazily rebased row
+// reference (one FADD2, or one FFMA2 that also undoes the fp16 scaling) ->
+// MUFU.EX2 (a few per chunk as an FMA-pipe polynomial) -> sum.
 //
 // Warp roles (one CTA per SM, 128 rows x one column chunk):
-//   warp 0      TMA producer: 1-D bulk copies of prepacked B' tiles (56 KB for
-//               KD=16) into a kTcStages-deep shared-memory ring (mbarrier
-//               full/empty); three stages keep two tiles of L2/DRAM latency
-//               in flight ahead of the MMA (the whole 2^20-column B' set,
-//               235 MB, does not fit the 126 MB L2)
+//   warp 0      TMA producer: 1-D bulk copies of prepacked B' tiles into a
+//               kTcStages-deep shared-memory ring (mbarrier full/empty); three
+//               stages keep two tiles of L2/DRAM latency in flight ahead of
+//               the MMA (column chunks of 48 MB keep a chunk's tiles in L2)
 //   warp 1      TMEM allocator + MMA issuer: one elected lane issues
-//               tcgen05.mma.kind::tf32 (M=128, N=256, K=8 per instruction) and
-//               tcgen05.commit to release the smem stage and publish the tile
+//               tcgen05.mma (M=128, N=256) and tcgen05.commit to release the
+//               smem stage and publish the tile
 //   warps 2..   EPI epilogue warps: warp w reads TMEM lane quadrant w%4 (32
 //               rows) and column part (w-2)/4 of each tile (32x32b.x32 loads,
 //               the next chunk's load in flight while the current is consumed)
 // Operands use the canonical K-major no-swizzle layout: 8-row x 16-byte core
 // matrices, SBO = 128 B between 8-row groups, LBO = rows*16 B between the two
-// 16-byte K chunks of one K=8 MMA step.
+// 16-byte K chunks of one MMA step.
 #pragma once
 
 #include <cuda_fp16.h>
