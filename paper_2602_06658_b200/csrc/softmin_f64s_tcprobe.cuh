@@ -61,7 +61,9 @@ struct TcpLayout {
 // 16). Measured at C4 2^20: 70 ms per probe with a 3-deep ring (the epilogue
 // warps waiting on the MMA warp waiting on the copies), 54 ms with 16. Also
 // measured, and slower (70 ms): all 16 epilogue warps taking 64 columns of
-// every stage with a named barrier per quadrant to join the partial minima.
+// every stage with a named barrier per quadrant to join the partial minima;
+// 64-column TMEM loads (x64) instead of 32-column ones (73 vs 67 ms per probe
+// sweep, and spills at kd + sq = 33).
 template <int KX, int TD>
 constexpr int tcp_ring() {
   constexpr int a = TcpLayout<KX>::kATileBytes, b = TcpLayout<KX>::kChunks * TD * 16;
