@@ -110,6 +110,10 @@ __global__ void __launch_bounds__(128) plan_reduce_ctr_kernel(const PlanReduceCt
       if (g8 + h < ng8 && a.need8[(g8 + h) * ntiles + t]) return true;
     return false;
   };
+  // ... and a stage the CTA walks is needed by some of them only: this row's own
+  // group decides whether it takes part (warp-uniform: the groups are multiples
+  // of 32 rows; at 32-row groups a CTA's union is ~4x what each warp needs)
+  const uint8_t* mine8 = use8 && live && a.grows > 0 ? a.need8 + (i / a.grows) * ntiles : nullptr;
   auto next_needed = [&](int t) {
     if (need)
       while (t < ntiles && !(need[t] & vote)) ++t;
@@ -139,8 +143,9 @@ __global__ void __launch_bounds__(128) plan_reduce_ctr_kernel(const PlanReduceCt
     mbar_wait(&bars[sb], (it >> 1) & 1);
     const double* rec = smem_k4 + sb * (SM::kRec + SM::kAcc);
     const double* acr = rec + SM::kRec;
+    const int jend = (use8 && (!mine8 || !mine8[t])) ? 0 : TILE;  // (dead rows of an F64S plan skip too)
 #pragma unroll 1
-    for (int j = 0; j < TILE; j += G) {
+    for (int j = 0; j < jend; j += G) {
       double q[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
