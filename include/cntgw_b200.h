@@ -226,6 +226,14 @@ int cntgw_select_order(const double* gamma, int de, const int64_t* order_if_zero
 int cntgw_prep_cols_f64s(const cntgw_sweep_state* st, int kd, int sq_flag, const double* feat, int64_t ld,
                          const double* sq, const double* pot, const double* log2w, const int64_t* order,
                          int64_t m, void* rec, void* stream);
+/* The same pack for a caller that owns a whole loop over fixed column features
+ * (sinkhorn.py:222-251: only the potentials change between sweeps): the first
+ * sweep of the loop (st->sweep <= 1) and every sweep of an annealed loop
+ * (st->anneal_from > 0: lam changes) pack everything, the others rewrite the
+ * bias column -(lam (pot - s^2) + log2 w) alone. Same arguments. */
+int cntgw_update_cols_f64s(const cntgw_sweep_state* st, int kd, int sq_flag, const double* feat, int64_t ld,
+                           const double* sq, const double* pot, const double* log2w, const int64_t* order,
+                           int64_t m, void* rec, void* stream);
 /* Workspace bytes of one half-update: split-column partials and, for
  * CNTGW_F32C, the block-sparse plan. The F32C part carries state from call to
  * call (the plan and its key, see above); a caller may share one workspace

@@ -108,6 +108,8 @@ SIGNATURES = {
     "cntgw_prep_rows_f64s": (c_int, [c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "cntgw_prep_cols_f64s": (c_int, [c_vp, c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,
                                      c_vp, c_vp]),
+    "cntgw_update_cols_f64s": (c_int, [c_vp, c_int, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,
+                                     c_vp, c_vp]),
     "cntgw_plan_reduce_f64s": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp,
                                        c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,
                                        c_vp, c_vp, c_size_t, c_vp, c_size_t, c_vp]),

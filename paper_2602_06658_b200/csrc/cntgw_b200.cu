@@ -629,7 +629,7 @@ template <typename T>
 __global__ void prep_cols_kernel(const cntgw_sweep_state* st, int kd, int sq_flag, int stride,
                                  const T* feat, int64_t ld, const T* sq, const double* pot,
                                  const double* log2w, int64_t m, int64_t mpad, T* rec,
-                                 const int64_t* order = nullptr) {
+                                 const int64_t* order = nullptr, int within_loop = 0) {
   const int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (jj >= mpad) return;
   T* r = rec + jj * stride;
@@ -637,6 +637,16 @@ __global__ void prep_cols_kernel(const cntgw_sweep_state* st, int kd, int sq_fla
   const bool f64 = sizeof(T) == 8;
   const double lam = f64 ? st->lam_d : (double)st->lam;
   const double sl = f64 ? st->sqrt_lam_d : (double)st->sqrt_lam;
+  // within a loop (same features, same lam: no annealing) only the potential moves:
+  // rewrite the bias column alone (cntgw_update_cols_f64s)
+  if (within_loop && st->sweep > 1 && !(st->anneal_from > 0.0)) {
+    if (jj < m) {
+      double beta = lam * (pot ? pot[j] : 0.0) + log2w[j];
+      if (sq_flag && f64) beta -= lam * (double)sq[j] * (double)sq[j];
+      r[kd + sq_flag] = (T)(-beta);
+    }
+    return;
+  }
   if (jj < m) {
     const T two_lam = (T)(2.0 * lam);
     for (int k = 0; k < kd; ++k) r[k] = -two_lam * feat[j * ld + k];
@@ -1174,6 +1184,19 @@ int cntgw_prep_cols_f64s(const cntgw_sweep_state* st, int kd, int sq_flag, const
   prep_cols_kernel<double><<<(unsigned)((mpad + 255) / 256), 256, 0, as_stream(stream)>>>(
       st, kd, sq_flag ? 1 : 0, stride, feat, ld, sq, pot, log2w, m, mpad, static_cast<double*>(rec), order);
   return check_launch("prep_cols_f64s");
+}
+
+int cntgw_update_cols_f64s(const cntgw_sweep_state* st, int kd, int sq_flag, const double* feat, int64_t ld,
+                           const double* sq, const double* pot, const double* log2w, const int64_t* order,
+                           int64_t m, void* rec, void* stream) {
+  if (!st || !feat || !log2w || !rec || m < 1 || (sq_flag && !sq))
+    return fail(CNTGW_EINVAL, "update_cols_f64s: bad arguments");
+  const int stride = cntgw_col_stride(CNTGW_F64S, kd, sq_flag);
+  if (stride < 0) return stride;
+  const int64_t mpad = cntgw_cols_padded(m);
+  prep_cols_kernel<double><<<(unsigned)((mpad + 255) / 256), 256, 0, as_stream(stream)>>>(
+      st, kd, sq_flag ? 1 : 0, stride, feat, ld, sq, pot, log2w, m, mpad, static_cast<double*>(rec), order, 1);
+  return check_launch("update_cols_f64s");
 }
 
 /* ---- K4 on the centred path's block-sparse plan (reduce_ctr.cuh) ---- */

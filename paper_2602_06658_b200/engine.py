@@ -374,8 +374,9 @@ class HalfUpdate:
         wsb = max(LIB.cntgw_softmin_workspace(p, rows.n, cols.n, self.kd, int(self.sq)) for p in precs)
         self.ws = torch.empty(max(int(wsb), 16), dtype=torch.uint8, device=dev)
         self.f64s_rows = None
-        # CNTGW_F64S: the rows block (order | features | s) is fixed within a loop; a driver that
-        # owns the loop gathers it once (hoist_rows) instead of once per half-update
+        # CNTGW_F64S: the rows block (order | features | s) and the columns' feature records are
+        # fixed within a loop; a driver that owns the loop gathers the rows once (hoist_rows)
+        # instead of once per half-update and lets pack() rewrite only the bias column
         self.rows_hoisted = False
         self.prec = prec  # (the setter sizes the F64S buffers: after the fields above)
 
@@ -407,7 +408,10 @@ class HalfUpdate:
                  c.locality().data_ptr(), c.n, self.ctr_cols.data_ptr(), _stream())
             return
         if prec == F64S:
-            call("cntgw_prep_cols_f64s", state.ptr, self.kd, int(self.sq), c.feat64.data_ptr(), self.kd,
+            # (hoisted: the owner of the loop guarantees fixed column features, so after the
+            # loop's first sweep only the bias column is rewritten)
+            call("cntgw_update_cols_f64s" if self.rows_hoisted else "cntgw_prep_cols_f64s",
+                 state.ptr, self.kd, int(self.sq), c.feat64.data_ptr(), self.kd,
                  _p(c.sq64 if self.sq else None), _p(pot_cols), c.log2w.data_ptr(),
                  c.plan_order().data_ptr(), c.n, self.rec.data_ptr(), _stream())
             return
