@@ -111,6 +111,7 @@ struct KernelPick {
   void* tcp_stats_fn = nullptr;
   void* tcp_pack_fn = nullptr;
   int tcp_threads = 0;
+  int tcp_tile = 0;              //   columns per probe tile (a whole number of plan stages)
   size_t tcp_smem = 0;
   size_t tcp_stage_bytes = 0;
 };
@@ -140,13 +141,15 @@ KernelPick f64s_variant() {
   }
   {
     using TL = TcpLayout<KD + SQ>;
-    constexpr int NB = 512 / TD < 4 ? 512 / TD : 4;
-    k.tcp_fn = (void*)f64s_tcp_kernel<KD + SQ, TD>;
+    constexpr int PT = TD < 128 ? 128 : TD;  // probe tile: two 64-column stages per MMA tile
+    constexpr int NB = 512 / PT < 4 ? 512 / PT : 4;
+    k.tcp_fn = (void*)f64s_tcp_kernel<KD + SQ, PT, TD>;
     k.tcp_stats_fn = (void*)f64s_tcp_stats_kernel<KD + SQ>;
     k.tcp_pack_fn = (void*)f64s_tcp_pack_kernel<KD + SQ>;
     k.tcp_threads = 64 + 128 * NB;
-    k.tcp_stage_bytes = (size_t)TL::kChunks * TD * 16;
-    k.tcp_smem = (size_t)TL::kATileBytes + tcp_ring<KD + SQ, TD>() * k.tcp_stage_bytes;
+    k.tcp_tile = PT;
+    k.tcp_stage_bytes = (size_t)TL::kChunks * PT * 16;
+    k.tcp_smem = (size_t)TL::kATileBytes + tcp_ring<KD + SQ, PT>() * k.tcp_stage_bytes;
     if (TL::kP > k.probe_p) k.probe_p = TL::kP;
   }
   return k;
@@ -433,23 +436,24 @@ int f64s_probe(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl,
         pl.full, rows, n, kd, sq, pl.sbound, stages, pl.nan);
     f64s_probe_gate_kernel<<<1, 1, 0, s>>>(pl.full, pl.nan, pl.probe_ok, pl.slack);
     f64s_tcp_scales_kernel<<<1, 1, 0, s>>>(pl.probe_ok, pl.sbound, stages);
+    const int ptiles = (int)(mpad / k.tcp_tile);
     {
       void* args[] = {(void*)&pl.probe_ok, (void*)&rec,   (void*)&stride,    (void*)&m,
-                      (void*)&k.f64s_tile, (void*)&tiles, (void*)&pl.sbound, (void*)&stages};
-      const cudaError_t e = cudaLaunchKernel(k.tcp_pack_fn, dim3(l.stages), dim3(128), args, 0, s);
+                      (void*)&k.tcp_tile,  (void*)&tiles, (void*)&pl.sbound, (void*)&stages};
+      const cudaError_t e = cudaLaunchKernel(k.tcp_pack_fn, dim3(ptiles), dim3(128), args, 0, s);
       if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(CNTGW_ECUDA, "f64s tc probe pack: %s", cudaGetErrorString(e));
       }
     }
     {
-      // stage tiles in chunks of <= 48 MB (L2), at least ~2 waves of CTAs
+      // probe tiles in chunks of <= 48 MB (L2), at least ~2 waves of CTAs
       const int64_t rt = (n + kTcRows - 1) / kTcRows;
       const int64_t fit = std::max<int64_t>(1, ((int64_t)48 << 20) / (int64_t)k.tcp_stage_bytes);
-      int chunks = (int)((l.stages + fit - 1) / fit);
-      chunks = (int)std::max<int64_t>(chunks, std::min<int64_t>(l.stages, (2 * num_sms() + rt - 1) / rt));
-      const int cs = (l.stages + chunks - 1) / chunks;
-      chunks = (l.stages + cs - 1) / cs;
+      int chunks = (int)((ptiles + fit - 1) / fit);
+      chunks = (int)std::max<int64_t>(chunks, std::min<int64_t>(ptiles, (2 * num_sms() + rt - 1) / rt));
+      const int cs = (ptiles + chunks - 1) / chunks;
+      chunks = (ptiles + cs - 1) / cs;
       cudaFuncSetAttribute(k.tcp_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.tcp_smem);
       void* args[] = {(void*)&pl.probe_ok, (void*)&rows,   (void*)&n,  (void*)&kd,      (void*)&tiles,
                       (void*)&pl.sbound,   (void*)&stages, (void*)&cs, (void*)&pl.tmin, (void*)&pl.slack};

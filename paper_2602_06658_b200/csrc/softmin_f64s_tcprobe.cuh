@@ -235,16 +235,21 @@ __global__ void __launch_bounds__(128) f64s_tcp_pack_kernel(const int* probe_ok,
   }
 }
 
-// The probe: one CTA = 128 ordered rows over one chunk of stages. Warp 0
-// streams the fp16 stage tiles (bulk copies into a 3-slot ring), warp 1 issues
-// the MMAs into NB = min(4, 512 / TD) TMEM accumulators of TD columns, and
-// 4 NB epilogue warps (TMEM lane quadrant q = warp % 4, accumulator p) take
-// the minimum of every NB-th stage.
-template <int KX, int TD>
+// The probe: one CTA = 128 ordered rows over one chunk of probe tiles. A probe
+// tile is TD columns = TD / SD plan stages (SD: the plan's stage width; 64-column
+// stages are probed two per 128-column MMA tile: half the MMA instructions).
+// Warp 0 streams the fp16 tiles (bulk copies into the ring), warp 1 issues the
+// MMAs into NB = min(4, 512 / TD) TMEM accumulators of TD columns, and 4 NB
+// epilogue warps (TMEM lane quadrant q = warp % 4, accumulator p) take the
+// stage minima of every NB-th tile. `stages` counts plan stages, `chunk_tiles`
+// probe tiles per blockIdx.y.
+template <int KX, int TD, int SD = TD>
 __global__ void __launch_bounds__(64 + 128 * (512 / TD < 4 ? 512 / TD : 4), 1)
     f64s_tcp_kernel(const int* probe_ok, const void* rows_block, int64_t n, int kd, const __half* tiles,
-                    float* sbound, int stages, int chunk_stages, float* tmin, float* slack) {
+                    float* sbound, int stages, int chunk_tiles, float* tmin, float* slack) {
   using L = TcpLayout<KX>;
+  static_assert(TD % SD == 0 && SD % 32 == 0, "a probe tile is a whole number of plan stages");
+  constexpr int kSub = TD / SD;  // plan stages per probe tile
   constexpr int NB = 512 / TD < 4 ? 512 / TD : 4;
   constexpr int kBStageBytes = L::kChunks * TD * 16;
   constexpr int kTcpStages = tcp_ring<KX, TD>();
@@ -259,8 +264,8 @@ __global__ void __launch_bounds__(64 + 128 * (512 / TD < 4 ? 512 / TD : 4), 1)
   char* sB = smem_tcp + L::kATileBytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row0 = (int64_t)blockIdx.x * kTcRows;
-  const int t0 = blockIdx.y * chunk_stages;
-  const int nt = min(stages - t0, chunk_stages);
+  const int t0 = blockIdx.y * chunk_tiles;
+  const int nt = min(stages / kSub - t0, chunk_tiles);
   const TcpHeader* hdr = tcp_header(sbound, stages);
 
   if (threadIdx.x == 0) {
@@ -377,13 +382,17 @@ __global__ void __launch_bounds__(64 + 128 * (512 / TD < 4 ? 512 / TD : 4), 1)
         }
 #pragma unroll
         for (int u = 0; u < 32; u += 2) m4[(u >> 1) & 3] = fmin3f(m4[(u >> 1) & 3], cur[u], cur[u + 1]);
+        if ((c + 1) % (SD / 32) == 0) {  // a plan stage is complete
+          const int stage = (t0 + t) * kSub + c / (SD / 32);
+          const float mn = fminf(fminf(m4[0], m4[1]), fminf(m4[2], m4[3]));
+          const float2 sb = __ldg(reinterpret_cast<const float2*>(sbound) + stage);
+          const float e = __fmaf_ru(__fmaf_ru(na, sb.x, sb.y), kE, floor_e);
+          smax = fmaxf(smax, e);
+          if (i < n) tmin[i * stages + stage] = __fsub_rd(mn * inv_sig, e);
+          m4[0] = m4[1] = m4[2] = m4[3] = CUDART_INF_F;
+        }
         if (c + 1 < TD / 32) tmem_wait_ld();
       }
-      const float mn = fminf(fminf(m4[0], m4[1]), fminf(m4[2], m4[3]));
-      const float2 sb = __ldg(reinterpret_cast<const float2*>(sbound) + (t0 + t));
-      const float e = __fmaf_ru(__fmaf_ru(na, sb.x, sb.y), kE, floor_e);
-      smax = fmaxf(smax, e);
-      if (i < n) tmin[i * stages + t0 + t] = __fsub_rd(mn * inv_sig, e);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, o));

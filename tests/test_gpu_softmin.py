@@ -405,6 +405,39 @@ def test_f64s_measured_plan_matches_dense_loop(env, k, anneal, monkeypatch):
     assert _rel(got[rows], want) < 5e-7
 
 
+@pytest.mark.parametrize("anneal", [None, 0.05], ids=["fixed", "annealed"])
+def test_f64s_hoisted_loop_equals_per_call_packing(env, anneal):
+    """A driver that owns a loop gathers the F64S rows block once and lets
+    pack() rewrite only the bias column after the first sweep
+    (cntgw_update_cols_f64s; every sweep packs everything when lam is
+    annealed): bit-identical to gathering and packing on every half-update."""
+    P, engine, S, O, torch, dev = env
+    from paper_2602_06658_b200._native import F64S
+
+    rng = np.random.default_rng(17)
+    n, m, k = 1800, 2600, 8
+    src = engine.Side.make(rng.standard_normal((n, k)) * 0.6, rng.random(n) * 4.0, np.full(n, 1 / n), dev, k)
+    tgt = engine.Side.make(rng.standard_normal((m, k)) * 0.6, rng.random(m) * 4.0, np.full(m, 1 / m), dev, k)
+    pots = [engine.to_dev64(rng.standard_normal(m) * (2.0 + s), dev) for s in range(4)]
+    outs = {}
+    for hoist in (False, True):
+        op = engine.HalfUpdate(src, tgt, True)
+        op.prec = F64S
+        st = engine.SweepState(dev)
+        st.init(2.5e-3, anneal, None, 8, "symmetrized")
+        if hoist:
+            op.hoist_rows()
+        res = []
+        for pot in pots:
+            st.begin()
+            out = torch.empty(n, dtype=torch.float64, device=dev)
+            op(st, pot, out, skip=False)
+            res.append(out.cpu().numpy())
+        outs[hoist] = res
+    for a_, b_ in zip(outs[False], outs[True]):
+        assert np.array_equal(a_, b_)
+
+
 @pytest.mark.parametrize("k", [3, 32])
 @pytest.mark.parametrize("zero_side", ["rows", "cols", "none"])
 def test_f64s_vanishing_dot_term(env, k, zero_side, monkeypatch):
