@@ -814,7 +814,7 @@ def egw_objective(gamma, coupling, src, tgt, eps: float) -> float:
         # _cnt_reductions (solvers.py:227-256) as device passes: pi Y and pi s_y
         # from K4, KL from the potentials identity (plan.plan_sums)
         r, pi_y, pi_s, _ = _plan_pass(coupling, src, tgt)
-        x = torch.as_tensor(np.asarray(src.features), device=pi_y.device)
+        x = torch.as_tensor(np.array(src.features, dtype=np.float64), device=pi_y.device)
         xt_pi_y = (x.t() @ pi_y).cpu().numpy()
         sigma_ss = float((torch.as_tensor(_half_sq(src), device=pi_y.device) * pi_s).sum())
         kl = kl_divergence(coupling)

@@ -90,6 +90,26 @@ def test_c1_potentials_and_loss(c1):
     assert _rel(res.coupling.cost._z, gold["zbar"]) < TOL
 
 
+@pytest.mark.parametrize("device_loop", ["1", "0"], ids=["captured", "host-loop"])
+def test_c1_forced_f64s_path(P, device_loop, monkeypatch):
+    """The whole C1 solve forced onto CNTGW_F64S (probe, measured plan, the
+    Gamma = 0 fast path of the first step, rows block gathered once and only
+    the bias column repacked within a thresholded loop), as one captured graph
+    and through the host loop: same decisions, potentials and loss as the
+    reference."""
+    gold = golden("c1_solve")
+    src, tgt = _measures(P, gold)
+    monkeypatch.setenv("CNTGW_PRECISION", "f64s")
+    monkeypatch.setenv("CNTGW_DEVICE_LOOP", device_loop)
+    res = P.solve_cnt_gw(src, tgt, P.make_config(0.01, threshold=1e-5, max_inner=200, max_outer=20))
+    assert res.trace.inner_iters == gold["inner_iters"].tolist()
+    assert res.converged == bool(gold["converged"])
+    assert _rel(res.coupling.f, gold["f"]) < TOL
+    assert _rel(res.coupling.g, gold["g"]) < TOL
+    assert abs(res.value - float(gold["value"])) <= TOL * abs(float(gold["value"]))
+    assert _rel(res.gamma, gold["gamma"]) < TOL
+
+
 def test_c1_marginal_err_trace(c1):
     gold, res = c1
     got, want = np.array(res.trace.marginal_errs), gold["marginal_err"]
