@@ -409,62 +409,62 @@ int f64s_revote(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl
   return f64s_vote(k, l, pl, st, rec, kd, sq, n, m, s, schedule, nullptr, skip);
 }
 
-// The fp32 probe of a dense measurement (softmin_f64s_probe.cuh), all gated on
-// the device flags: prep + row check (iff *full), gate, probe, reduce and
-// commit of its plan, then the re-vote on it. Leaves the sweep non-measuring
-// (or a partial measurement when the probe's plan keeps too much).
-int f64s_probe(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl, const cntgw_sweep_state* st,
-               int skip, const double* rec, int kd, int sq, const void* rows, const void* cols, int64_t n, int64_t m,
-               cudaStream_t s) {
-  const int stride = cntgw_col_stride(CNTGW_F64S, kd, sq);
-  const int64_t mpad = (m + kColTile - 1) / kColTile * kColTile;
-  cudaMemsetAsync(pl.nan, 0, sizeof(int), s);
-  if (f64s_tcp_enabled(k)) {  // the tensor-core probe (softmin_f64s_tcprobe.cuh)
-    int stages = l.stages;
-    __half* tiles = reinterpret_cast<__half*>(pl.rec32);
-    f64s_tcp_begin_kernel<<<1, 1, 0, s>>>(pl.sbound, stages);
-    {
-      void* args[] = {(void*)&pl.full, (void*)&rec,       (void*)&stride, (void*)&m,
-                      (void*)&k.f64s_tile, (void*)&pl.sbound, (void*)&stages, (void*)&pl.nan};
-      const cudaError_t e = cudaLaunchKernel(k.tcp_stats_fn, dim3(l.stages), dim3(128), args, 0, s);
-      if (e != cudaSuccess) {
-        cudaGetLastError();
-        return fail(CNTGW_ECUDA, "f64s tc probe stats: %s", cudaGetErrorString(e));
-      }
+// The probe of a dense measurement, all gated on the device flags: statistics
+// / prep + row check (iff *full), gate, probe, reduce and commit of its plan,
+// then the re-vote on it. Leaves the sweep non-measuring (or a partial
+// measurement when the probe's plan keeps too much).
+// -- the tensor-core probe (softmin_f64s_tcprobe.cuh), any width
+int f64s_probe_tc(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl, const double* rec, int stride,
+                  int kd, int sq, const void* rows, int64_t n, int64_t m, int64_t mpad, cudaStream_t s) {
+  int stages = l.stages;
+  __half* tiles = reinterpret_cast<__half*>(pl.rec32);
+  f64s_tcp_begin_kernel<<<1, 1, 0, s>>>(pl.sbound, stages);
+  {
+    void* args[] = {(void*)&pl.full,     (void*)&rec,       (void*)&stride, (void*)&m,
+                    (void*)&k.f64s_tile, (void*)&pl.sbound, (void*)&stages, (void*)&pl.nan};
+    const cudaError_t e = cudaLaunchKernel(k.tcp_stats_fn, dim3(l.stages), dim3(128), args, 0, s);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(CNTGW_ECUDA, "f64s tc probe stats: %s", cudaGetErrorString(e));
     }
-    f64s_tcp_rows_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1184), 256, 0, s>>>(
-        pl.full, rows, n, kd, sq, pl.sbound, stages, pl.nan);
-    f64s_probe_gate_kernel<<<1, 1, 0, s>>>(pl.full, pl.nan, pl.probe_ok, pl.slack);
-    f64s_tcp_scales_kernel<<<1, 1, 0, s>>>(pl.probe_ok, pl.sbound, stages);
-    const int ptiles = (int)(mpad / k.tcp_tile);
-    {
-      void* args[] = {(void*)&pl.probe_ok, (void*)&rec,   (void*)&stride,    (void*)&m,
-                      (void*)&k.tcp_tile,  (void*)&tiles, (void*)&pl.sbound, (void*)&stages};
-      const cudaError_t e = cudaLaunchKernel(k.tcp_pack_fn, dim3(ptiles), dim3(128), args, 0, s);
-      if (e != cudaSuccess) {
-        cudaGetLastError();
-        return fail(CNTGW_ECUDA, "f64s tc probe pack: %s", cudaGetErrorString(e));
-      }
+  }
+  f64s_tcp_rows_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 8 * num_sms()), 256, 0, s>>>(
+      pl.full, rows, n, kd, sq, pl.sbound, stages, pl.nan);
+  f64s_probe_gate_kernel<<<1, 1, 0, s>>>(pl.full, pl.nan, pl.probe_ok, pl.slack);
+  f64s_tcp_scales_kernel<<<1, 1, 0, s>>>(pl.probe_ok, pl.sbound, stages);
+  const int ptiles = (int)(mpad / k.tcp_tile);
+  {
+    void* args[] = {(void*)&pl.probe_ok, (void*)&rec,   (void*)&stride,    (void*)&m,
+                    (void*)&k.tcp_tile,  (void*)&tiles, (void*)&pl.sbound, (void*)&stages};
+    const cudaError_t e = cudaLaunchKernel(k.tcp_pack_fn, dim3(ptiles), dim3(128), args, 0, s);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(CNTGW_ECUDA, "f64s tc probe pack: %s", cudaGetErrorString(e));
     }
-    {
-      // probe tiles in chunks of <= 48 MB (L2), at least ~2 waves of CTAs
-      const int64_t rt = (n + kTcRows - 1) / kTcRows;
-      const int64_t fit = std::max<int64_t>(1, ((int64_t)48 << 20) / (int64_t)k.tcp_stage_bytes);
-      int chunks = (int)((ptiles + fit - 1) / fit);
-      chunks = (int)std::max<int64_t>(chunks, std::min<int64_t>(ptiles, (2 * num_sms() + rt - 1) / rt));
-      const int cs = (ptiles + chunks - 1) / chunks;
-      chunks = (ptiles + cs - 1) / cs;
-      cudaFuncSetAttribute(k.tcp_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.tcp_smem);
-      void* args[] = {(void*)&pl.probe_ok, (void*)&rows,   (void*)&n,  (void*)&kd,      (void*)&tiles,
-                      (void*)&pl.sbound,   (void*)&stages, (void*)&cs, (void*)&pl.tmin, (void*)&pl.slack};
-      const cudaError_t e =
-          cudaLaunchKernel(k.tcp_fn, dim3((unsigned)rt, (unsigned)chunks), dim3(k.tcp_threads), args, k.tcp_smem, s);
-      if (e != cudaSuccess) {
-        cudaGetLastError();
-        return fail(CNTGW_ECUDA, "f64s tc probe: %s", cudaGetErrorString(e));
-      }
-    }
-  } else {
+  }
+  // probe tiles in chunks of <= 48 MB (L2), at least ~2 waves of CTAs
+  const int64_t rt = (n + kTcRows - 1) / kTcRows;
+  const int64_t fit = std::max<int64_t>(1, ((int64_t)48 << 20) / (int64_t)k.tcp_stage_bytes);
+  int chunks = (int)((ptiles + fit - 1) / fit);
+  chunks = (int)std::max<int64_t>(chunks, std::min<int64_t>(ptiles, (2 * num_sms() + rt - 1) / rt));
+  const int cs = (ptiles + chunks - 1) / chunks;
+  chunks = (ptiles + cs - 1) / cs;
+  cudaFuncSetAttribute(k.tcp_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.tcp_smem);
+  void* args[] = {(void*)&pl.probe_ok, (void*)&rows,   (void*)&n,  (void*)&kd,      (void*)&tiles,
+                  (void*)&pl.sbound,   (void*)&stages, (void*)&cs, (void*)&pl.tmin, (void*)&pl.slack};
+  const cudaError_t e =
+      cudaLaunchKernel(k.tcp_fn, dim3((unsigned)rt, (unsigned)chunks), dim3(k.tcp_threads), args, k.tcp_smem, s);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CNTGW_ECUDA, "f64s tc probe: %s", cudaGetErrorString(e));
+  }
+  return CNTGW_OK;
+}
+
+// -- the fp32 FFMA2 probe (softmin_f64s_probe.cuh), kd + sq <= 8
+int f64s_probe_ffma(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl, const cntgw_sweep_state* st,
+                    int skip, const double* rec, int stride, int kd, int sq, const void* rows, int64_t n, int64_t m,
+                    cudaStream_t s) {
   {
     void* args[] = {(void*)&pl.full, (void*)&rec, (void*)&stride, (void*)&m, (void*)&k.f64s_tile,
                     (void*)&pl.rec32, (void*)&pl.sbound, (void*)&pl.nan};
@@ -474,26 +474,35 @@ int f64s_probe(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl,
       return fail(CNTGW_ECUDA, "f64s probe prep: %s", cudaGetErrorString(e));
     }
   }
-  f64s_probe_rows_check_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1184), 256, 0, s>>>(
+  f64s_probe_rows_check_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 8 * num_sms()), 256, 0, s>>>(
       pl.full, rows, n, kd, sq, pl.nan);
   f64s_probe_gate_kernel<<<1, 1, 0, s>>>(pl.full, pl.nan, pl.probe_ok, pl.slack);
-  {
-    const int64_t rt = (n + k.probe_rows - 1) / k.probe_rows;
-    // enough CTAs for ~4 waves of 2 per SM: split the stages into chunks
-    int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(l.stages, (148 * 8 + rt - 1) / rt));
-    const int cs = (l.stages + chunks - 1) / chunks;
-    chunks = (l.stages + cs - 1) / cs;
-    const size_t smem = (size_t)2 * k.f64s_tile * k.probe_p * sizeof(float);
-    int stages = l.stages;
-    void* args[] = {(void*)&st, (void*)&skip, (void*)&pl.probe_ok, (void*)&rows, (void*)&n, (void*)&pl.rec32,
-                    (void*)&pl.sbound, (void*)&stages, (void*)&cs, (void*)&pl.tmin, (void*)&pl.slack};
-    const cudaError_t e = cudaLaunchKernel(k.probe_fn, dim3((unsigned)rt, (unsigned)chunks), dim3(128), args, smem, s);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return fail(CNTGW_ECUDA, "f64s probe: %s", cudaGetErrorString(e));
-    }
+  const int64_t rt = (n + k.probe_rows - 1) / k.probe_rows;
+  // enough CTAs for ~4 waves of 2 per SM: split the stages into chunks
+  int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(l.stages, (8 * num_sms() + rt - 1) / rt));
+  const int cs = (l.stages + chunks - 1) / chunks;
+  chunks = (l.stages + cs - 1) / cs;
+  const size_t smem = (size_t)2 * k.f64s_tile * k.probe_p * sizeof(float);
+  int stages = l.stages;
+  void* args[] = {(void*)&st, (void*)&skip, (void*)&pl.probe_ok, (void*)&rows, (void*)&n, (void*)&pl.rec32,
+                  (void*)&pl.sbound, (void*)&stages, (void*)&cs, (void*)&pl.tmin, (void*)&pl.slack};
+  const cudaError_t e = cudaLaunchKernel(k.probe_fn, dim3((unsigned)rt, (unsigned)chunks), dim3(128), args, smem, s);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CNTGW_ECUDA, "f64s probe: %s", cudaGetErrorString(e));
   }
-  }
+  return CNTGW_OK;
+}
+
+int f64s_probe(const KernelPick& k, const F64sPlanLayout& l, const F64sPlan& pl, const cntgw_sweep_state* st,
+               int skip, const double* rec, int kd, int sq, const void* rows, const void* cols, int64_t n, int64_t m,
+               cudaStream_t s) {
+  const int stride = cntgw_col_stride(CNTGW_F64S, kd, sq);
+  const int64_t mpad = (m + kColTile - 1) / kColTile * kColTile;
+  cudaMemsetAsync(pl.nan, 0, sizeof(int), s);
+  const int rc = f64s_tcp_enabled(k) ? f64s_probe_tc(k, l, pl, rec, stride, kd, sq, rows, n, m, mpad, s)
+                                     : f64s_probe_ffma(k, l, pl, st, skip, rec, stride, kd, sq, rows, n, m, s);
+  if (rc != CNTGW_OK) return rc;
   f64s_reduce_kernel<<<(unsigned)l.row_tiles, 256, f64s_reduce_smem(k, l.stages), s>>>(
       pl.probe_ok, pl.probe_ok, pl.tmin, pl.need, pl.range, n, l.stages, k.cta_rows, pl.gmin, pl.tstar, pl.rowmin,
       0.f, pl.slack);
