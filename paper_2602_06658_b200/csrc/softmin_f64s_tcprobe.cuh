@@ -173,8 +173,10 @@ __global__ void f64s_tcp_rows_kernel(const int* full, const void* rows_block, in
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nan, 1);
 }
 
-// (1 thread, after the gate) the scale exponents of this probe
-__global__ void f64s_tcp_scales_kernel(const int* probe_ok, float* sbound, int stages) {
+// (1 thread, after the gate) the scale exponents of this probe; magnitudes
+// whose scales would leave fp32's normal range make the probe stand down (the
+// dense fp64 measurement runs instead)
+__global__ void f64s_tcp_scales_kernel(int* probe_ok, float* sbound, int stages) {
   if (!*probe_ok) return;
   TcpHeader* h = tcp_header(sbound, stages);
   auto ex = [](uint32_t bits) {  // 2^e > value (0 for an all-zero side)
@@ -187,6 +189,8 @@ __global__ void f64s_tcp_scales_kernel(const int* probe_ok, float* sbound, int s
   h->esa = 14 - ea;
   h->esb = esig - (14 - ea);
   h->esig = esig;
+  auto bad = [](int k) { return k < -120 || k > 120; };
+  if (bad(h->esa) || bad(h->esb) || bad(esig) || bad(esig - 15)) *probe_ok = 0;
 }
 
 // one block per stage (gated on *probe_ok): the fp16 stage tile

@@ -99,6 +99,10 @@ __device__ __forceinline__ float pow2i(int k) {
   k = k < -126 ? -126 : (k > 127 ? 127 : k);
   return __int_as_float((127 + k) << 23);
 }
+// ... for a scale that must be exact: NaN (loud) when 2^k is not a normal fp32
+__device__ __forceinline__ float pow2i_exact(int k) {
+  return (k < -126 || k > 127) ? __int_as_float(0x7fc00000) : __int_as_float((127 + k) << 23);
+}
 
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
@@ -228,7 +232,7 @@ __global__ void prep_cols_tch_kernel(const cntgw_sweep_state* st, const float* f
   if (j < m) {
     const double lam = (double)st->lam;
     const float two_lam = (float)(2.0 * lam);
-    const float sb = pow2i(14 - tch_col_exp(*absmax, two_lam));
+    const float sb = pow2i_exact(14 - tch_col_exp(*absmax, two_lam));
     for (int k = 0; k < KD; ++k) {
       const float z = two_lam * feat[j * ld + k];
       const float zh = tf32_rna(z);
@@ -352,7 +356,7 @@ __global__ void __launch_bounds__(tc_threads(EPI), 1) softmin_tc_kernel(const So
       auto put = [&](int p, float v) { hA[(p >> 3) * (kTcRows * 8) + r * 8 + (p & 7)] = __float2half_rn(v); };
       const uint32_t absmax = *reinterpret_cast<const uint32_t*>(static_cast<const char*>(a.col_rec) +
                                                                  mpad * L::kRecBytes);
-      const float sa = pow2i(tch_col_exp(absmax, (float)(2.0 * (double)a.st->lam)) + 1);
+      const float sa = pow2i_exact(tch_col_exp(absmax, (float)(2.0 * (double)a.st->lam)) + 1);
       for (int k = h * (KD / kParts); k < (h + 1) * (KD / kParts); ++k) {
         const float x = i < a.n ? xf[i * a.ld_row + k] : 0.f;
         const float xh = tf32_rna(x);

@@ -438,6 +438,32 @@ def test_f64s_hoisted_loop_equals_per_call_packing(env, anneal):
         assert np.array_equal(a_, b_)
 
 
+def test_f64s_probe_stands_down_on_extreme_scales(env):
+    """Row features of magnitude 1e-37 would need a power-of-two scale beyond
+    fp32's normal range in the tcgen05 probe: it stands down and the sweep
+    measures in fp64 instead, with the dense path's results."""
+    P, engine, S, O, torch, dev = env
+    from paper_2602_06658_b200._native import F64, F64S
+
+    rng = np.random.default_rng(5)
+    n, m, k = 900, 1300, 3
+    src = engine.Side.make(rng.standard_normal((n, k)) * 1e-37, rng.random(n) * 1e-37, np.full(n, 1 / n), dev, k)
+    tgt = engine.Side.make(rng.standard_normal((m, k)), rng.random(m) * 3.0, np.full(m, 1 / m), dev, k)
+    pot = engine.to_dev64(rng.standard_normal(m) * 5.0, dev)
+    outs = {}
+    for name, prec in (("f64s", F64S), ("f64", F64)):
+        op = engine.HalfUpdate(src, tgt, True)
+        op.prec = prec
+        st = engine.SweepState(dev)
+        st.init(2.5e-3, None, None, 4, "symmetrized")
+        st.begin()
+        out = torch.empty(n, dtype=torch.float64, device=dev)
+        op(st, pot, out, skip=False)
+        outs[name] = out.cpu().numpy()
+    assert np.all(np.isfinite(outs["f64s"]))
+    assert _rel(outs["f64s"], outs["f64"]) < 5e-9
+
+
 @pytest.mark.parametrize("k", [3, 32])
 @pytest.mark.parametrize("zero_side", ["rows", "cols", "none"])
 def test_f64s_vanishing_dot_term(env, k, zero_side, monkeypatch):
