@@ -600,7 +600,10 @@ class SinkhornLoop:
 
     def _replay(self, f, g, mode, k):
         prec = tuple(getattr(op, "prec", None) for op in (self.fwd, self.bwd))
-        key = (f.data_ptr(), g.data_ptr(), mode, k, prec)
+        # (a graph captured with hoisted rows holds no row gather and bias-only column packs:
+        # it must not serve a caller that did not hoist)
+        hoisted = tuple(getattr(op, "rows_hoisted", False) for op in (self.fwd, self.bwd))
+        key = (f.data_ptr(), g.data_ptr(), mode, k, prec, hoisted)
         graph = self._graphs.get(key)
         if graph is None:
             side = torch.cuda.Stream()
