@@ -232,10 +232,18 @@ def tc_supported(kd: int, sq: bool) -> bool:
     return kd in (8, 16) and not sq
 
 
-# CNTGW_F64S (fp64 with a measured block-sparse plan) for cold problems the
-# centred path cannot take, from this many pairs per half-update (below it a
-# dense fp64 sweep takes milliseconds and the plan does not pay off)
-F64S_MIN_PAIRS = float(os.environ.get("CNTGW_F64S_MIN_PAIRS", 2.0 ** 34))
+# CNTGW_F64S (fp64 with a measured block-sparse plan) for cold problems, from
+# this many pairs per half-update: below it a dense fp64 sweep is cheaper than
+# the plan's ~15 small launches per half-update. Measured crossovers on the
+# cold laws (tools/gpu/r2_s3_45.sh, time per outer step): kd = 3 between
+# N = 8192 (dense 24 ms, F64S 35 ms) and 16384 (87 / 46 ms); kd = 32 between
+# N = 2048 (28 / 48 ms) and 4096 (52 / 30 ms); at N = 65536 / 32768 the plan
+# is 8x / 12x faster. CNTGW_F64S_MIN_PAIRS overrides.
+def f64s_min_pairs(kd: int) -> float:
+    env = os.environ.get("CNTGW_F64S_MIN_PAIRS")
+    if env is not None:
+        return float(env)
+    return 2.0 ** 24 if kd >= 16 else 2.0 ** 27
 
 
 def choose_precision(scale: float, kd: int = 0, sq: bool = True, ctr_deferred=None,
@@ -256,9 +264,8 @@ def choose_precision(scale: float, kd: int = 0, sq: bool = True, ctr_deferred=No
     if forced in ("f32c", "ctr"):
         return F32C if ctr_supported(kd, sq) else F64
     if scale >= F32_EXPONENT_LIMIT:
-        # large cold problems: fp64 with the measured block-sparse plan (C4 at
-        # 2^20: 79 s vs 157 s on the centred fp32 path, and fp64-exact terms)
-        if pairs >= F64S_MIN_PAIRS and os.environ.get("CNTGW_F64S", "1") != "0":
+        # cold problems past the crossover: fp64 with the measured block-sparse plan
+        if pairs >= f64s_min_pairs(kd) and os.environ.get("CNTGW_F64S", "1") != "0":
             return F64S
         if (ctr_deferred is not None and ctr_supported(kd, sq)
                 and os.environ.get("CNTGW_CTR", "1") != "0" and ctr_deferred() <= CTR_MAX_DEFERRED):
