@@ -189,8 +189,9 @@ int half_apply(cntgw_solver* s, Half& h, const double* pot, double* out, int ski
   Side& c = *h.cols;
   Side& r = *h.rows;
   if (prec == CNTGW_F64S) {
-    TRY(cntgw_prep_cols_f64s(s->st, kd, 1, c.feat64, kd, c.sq, pot, c.log2w, c.order, c.n, h.rec, st));
-    TRY(cntgw_prep_rows_f64s(kd, 1, r.feat64, kd, r.sq, r.order, r.n, h.f64s_rows, st));
+    // (the rows blocks are gathered once per loop in set_gamma; within a loop only the bias
+    // column of the records moves)
+    TRY(cntgw_update_cols_f64s(s->st, kd, 1, c.feat64, kd, c.sq, pot, c.log2w, c.order, c.n, h.rec, st));
     return cntgw_softmin(s->st, skip, prec, kd, 1, h.f64s_rows, kd, r.sq, nullptr, h.rec, r.n, c.n, out, mx, sm,
                          h.ws, h.ws_bytes, st);
   }
@@ -242,8 +243,13 @@ int set_gamma(cntgw_solver* s, const double* gamma, cudaStream_t st) {
   } else {  // cols: Gamma Y_j
     op = gamma, side = &s->tgt, feat = s->y, count = s->m, din = s->e, dout = s->d;
   }
-  return cntgw_apply_operator(op, dout, din, feat, din, count, side->feat64,
-                              s->cfg.precision == CNTGW_F32 ? side->feat32 : nullptr, s->kd, st);
+  TRY(cntgw_apply_operator(op, dout, din, feat, din, count, side->feat64,
+                           s->cfg.precision == CNTGW_F32 ? side->feat32 : nullptr, s->kd, st));
+  if (s->cfg.precision == CNTGW_F64S)  // new features: the F64S rows blocks of both half-updates
+    for (Half* h : {&s->fwd, &s->bwd})
+      TRY(cntgw_prep_rows_f64s(s->kd, 1, h->rows->feat64, s->kd, h->rows->sq, h->rows->order, h->rows->n,
+                               h->f64s_rows, st));
+  return CNTGW_OK;
 }
 
 // K2 tentative (skipped after a symmetrized threshold break), K4, K7
